@@ -1,0 +1,122 @@
+/*
+ * moa_b200.h — C ABI of the B200 backend for the MoA generalized inner/outer
+ * product (Raynolds & Mullin, arXiv 0907.0792).
+ *
+ * The boundary mirrors the reference backend's hot-loop contract
+ *
+ *   _ckernel.product_rows(res, a, b, noproc, rowsinred, elsinop,
+ *                         lstride, rstride, restride,
+ *                         combine_code, reduce_code, start, step)
+ *   (/root/reference/pkg/src/moaprod/_ckernel.pyx:75-88, Python twin
+ *    _purekernel.py:15-37, called only from kernel.py:164-165)
+ *
+ * argument for argument: the same loop bounds, the same flat strides, the same
+ * operation codes (ops.py:52-66) and the same row set start, start+step, ...
+ * The differences are the ones a device backend needs:
+ *   - res/a/b are DEVICE pointers (any allocation visible to the current
+ *     device; the caller owns them, as the reference's caller owns its numpy
+ *     buffers, kernel.py:149);
+ *   - an element type code (the reference is float64 only, arrays.py:77-78);
+ *   - a flags word: by default res is WRITE-ONLY and every result element is
+ *     folded from the reduce identity in registers, which is bit-identical to
+ *     the reference's identity prefill (kernel.py:149) followed by the
+ *     accumulate (_ckernel.pyx:51,70) but skips the prefill pass.  With
+ *     MOA_FLAG_ACCUMULATE the fold starts from res's current contents exactly
+ *     as the reference's product_rows does;
+ *   - a cudaStream_t (as void*) on which all work is enqueued; the call is
+ *     asynchronous with respect to the host, like any CUDA launch.
+ *
+ * Errors: 0 on success; MOA_E_* (< 0) for argument errors; a positive
+ * cudaError_t value when the CUDA runtime reports one.  moa_last_error()
+ * returns a thread-local message for the last failure on the calling thread.
+ * Shape/plan validation stays in the host layer (kernel.py:111-135 analogue),
+ * which raises the reference's exception classes before this is reached.
+ *
+ * All entry points are thread-safe and reentrant: there is no global mutable
+ * state apart from an atomic launch counter.
+ */
+#ifndef MOA_B200_H
+#define MOA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types (the reference has float64 only, arrays.py:77-78) */
+#define MOA_DTYPE_F64 0
+#define MOA_DTYPE_F32 1
+
+/* combine codes — identical to ops.py:52-59 and _ckernel.pyx:11-23 */
+#define MOA_COMBINE_ADD 0
+#define MOA_COMBINE_SUBTRACT 1
+#define MOA_COMBINE_MULTIPLY 2
+#define MOA_COMBINE_DIVIDE 3
+#define MOA_COMBINE_MIN 4
+#define MOA_COMBINE_MAX 5
+
+/* reduce codes — identical to ops.py:61-66 and _ckernel.pyx:26-34 */
+#define MOA_REDUCE_ADD 0
+#define MOA_REDUCE_MULTIPLY 1
+#define MOA_REDUCE_MIN 2
+#define MOA_REDUCE_MAX 3
+
+/* flags */
+#define MOA_FLAG_ACCUMULATE 1u /* fold into res's existing values (reference semantics) */
+#define MOA_FLAG_EXACT 2u      /* (multiply, add): reference rounding and fold order
+                                  (separate multiply and add, l ascending) instead of
+                                  the FP64 DMMA tensor-core path */
+
+/* argument errors */
+#define MOA_E_DTYPE (-1)
+#define MOA_E_OPCODE (-2)
+#define MOA_E_BOUNDS (-3) /* negative extent/stride, step < 1, start < 0 */
+#define MOA_E_NULL (-4)   /* null operand pointer with non-empty work */
+
+/*
+ * Replaces _ckernel.product_rows (_ckernel.pyx:75-88).  Computes, for every
+ * row i in {start, start+step, ...} below noproc and every j < elsinop,
+ *
+ *   res[i*restride + j] = fold_{l ascending < rowsinred} reduce(., combine(
+ *                             a[l + i*lstride], b[l*rstride + j]))
+ *
+ * starting from the reduce identity (default) or from res (ACCUMULATE).
+ * Bit-exact with the reference for every (combine, reduce) pair except
+ * (multiply, add) without MOA_FLAG_EXACT, which runs on the FP64 tensor cores
+ * with fused multiply-adds and is accurate to K*2^-52*max|A|*max|B|.
+ * float32 operands follow the reference's upcast (arrays.py:77-78): the result
+ * equals the reference's float64 result rounded to float32.
+ */
+int moa_product_rows(int dtype, void* res, const void* a, const void* b,
+                     int64_t noproc, int64_t rowsinred, int64_t elsinop,
+                     int64_t lstride, int64_t rstride, int64_t restride,
+                     int combine_code, int reduce_code,
+                     int64_t start, int64_t step,
+                     uint32_t flags, void* stream);
+
+/* Message for the last failing call on this thread ("" if none). */
+const char* moa_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int moa_abi_version(void);
+
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t moa_launch_count(void);
+
+/*
+ * Which kernel moa_product_rows would run for these arguments, as a static
+ * string ("outer", "fill", "dmma", "semiring_exact", "semiring_fast", "none").
+ * Host-only; launches nothing.  "semiring_fast" means the kernel that decides
+ * on the device, after a NaN/-0/inf pre-scan of the operands, whether the
+ * 3-input min/max fast loop is bit-exact for this data.
+ */
+const char* moa_plan_kernel(int dtype, int64_t noproc, int64_t rowsinred,
+                            int64_t elsinop, int combine_code, int reduce_code,
+                            uint32_t flags);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOA_B200_H */

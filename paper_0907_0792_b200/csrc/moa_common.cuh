@@ -1,0 +1,116 @@
+// Shared device definitions: the operation codes of the reference
+// (ops.py:52-66, _ckernel.pyx:11-34) as compile-time functors, the
+// accumulation type rule for float32 storage, and launch helpers.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace moa {
+
+enum Combine : int { C_ADD = 0, C_SUB = 1, C_MUL = 2, C_DIV = 3, C_MIN = 4, C_MAX = 5 };
+enum Reduce : int { R_ADD = 0, R_MUL = 1, R_MIN = 2, R_MAX = 3 };
+
+constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------------------
+// combine(x, y) with the reference's operand order (_ckernel.pyx:71: combine
+// gets the A element first).  Every arithmetic op is an explicit _rn intrinsic
+// so nvcc can never contract a combine with a following reduce into an FMA
+// (the reference is built with -ffp-contract=off, setup.py:14).
+// min/max are the reference's compare-and-select (ops.py:42-47), NOT fmin/fmax:
+// x if x < y else y keeps the second operand on NaN and on a +-0 tie.
+// ---------------------------------------------------------------------------
+template <int C> struct CombineOp;
+template <> struct CombineOp<C_ADD> {
+  static __device__ __forceinline__ double f(double x, double y) { return __dadd_rn(x, y); }
+  static __device__ __forceinline__ float f(float x, float y) { return __fadd_rn(x, y); }
+};
+template <> struct CombineOp<C_SUB> {
+  static __device__ __forceinline__ double f(double x, double y) { return __dsub_rn(x, y); }
+  static __device__ __forceinline__ float f(float x, float y) { return __fsub_rn(x, y); }
+};
+template <> struct CombineOp<C_MUL> {
+  static __device__ __forceinline__ double f(double x, double y) { return __dmul_rn(x, y); }
+  static __device__ __forceinline__ float f(float x, float y) { return __fmul_rn(x, y); }
+};
+template <> struct CombineOp<C_DIV> {
+  static __device__ __forceinline__ double f(double x, double y) { return __ddiv_rn(x, y); }
+  static __device__ __forceinline__ float f(float x, float y) { return __fdiv_rn(x, y); }
+};
+template <> struct CombineOp<C_MIN> {
+  template <typename T> static __device__ __forceinline__ T f(T x, T y) { return x < y ? x : y; }
+};
+template <> struct CombineOp<C_MAX> {
+  template <typename T> static __device__ __forceinline__ T f(T x, T y) { return x > y ? x : y; }
+};
+
+// reduce(acc, v): _ckernel.pyx:26-34 / ops.py:61-66; acc is the left operand.
+template <int R> struct ReduceOp;
+template <> struct ReduceOp<R_ADD> {
+  static __device__ __forceinline__ double f(double x, double y) { return __dadd_rn(x, y); }
+  static __device__ __forceinline__ float f(float x, float y) { return __fadd_rn(x, y); }
+  template <typename T> static __host__ __device__ constexpr T identity() { return T(0); }
+};
+template <> struct ReduceOp<R_MUL> {
+  static __device__ __forceinline__ double f(double x, double y) { return __dmul_rn(x, y); }
+  static __device__ __forceinline__ float f(float x, float y) { return __fmul_rn(x, y); }
+  template <typename T> static __host__ __device__ constexpr T identity() { return T(1); }
+};
+template <> struct ReduceOp<R_MIN> {
+  template <typename T> static __device__ __forceinline__ T f(T x, T y) { return x < y ? x : y; }
+  template <typename T> static __host__ __device__ T identity() { return T(__builtin_huge_val()); }
+};
+template <> struct ReduceOp<R_MAX> {
+  template <typename T> static __device__ __forceinline__ T f(T x, T y) { return x > y ? x : y; }
+  template <typename T> static __host__ __device__ T identity() { return T(-__builtin_huge_val()); }
+};
+
+// ---------------------------------------------------------------------------
+// Arithmetic type for a storage type.  The reference upcasts every operand to
+// float64 (arrays.py:77-78), so a float32 product must equal the float64
+// result rounded once to float32.  For a min/max reduce float32 arithmetic
+// already gives that (add/sub/mul/div of two floats rounded to float32 equals
+// the float64 op rounded to float32 — 53 >= 2*24+2 makes double rounding
+// innocuous — and a compare-select fold commutes with a monotone rounding), so
+// it stays in float32.  Sums and products of many terms do not commute with
+// rounding, so add/multiply reduces on float32 storage run in float64.
+// ---------------------------------------------------------------------------
+template <typename T, int R> struct AccType { using type = T; };
+template <> struct AccType<float, R_ADD> { using type = double; };
+template <> struct AccType<float, R_MUL> { using type = double; };
+
+template <typename To, typename From> __device__ __forceinline__ To convert(From x) { return To(x); }
+template <> __device__ __forceinline__ float convert<float, double>(double x) { return __double2float_rn(x); }
+
+// ---------------------------------------------------------------------------
+// operand special-value flags from the device pre-scan (semiring fast path)
+// ---------------------------------------------------------------------------
+enum SpecialBits : unsigned {
+  S_NAN = 1u, S_PINF = 2u, S_NINF = 4u, S_NZERO = 8u, S_PZERO = 16u
+};
+
+// Whether a fold with the hardware 3-input min/max (FMNMX3, which prefers the
+// non-NaN operand and may order +-0 arbitrarily) is bit-identical to the
+// reference's compare-select fold, given the special values that occur in A
+// and in B.  True iff no combine result can be NaN or -0.0: then the fold is
+// an exact min/max over ordered values and any association order gives the
+// same bits.
+__host__ __device__ inline bool fast_fold_is_exact(int combine, unsigned fa, unsigned fb) {
+  if ((fa | fb) & S_NAN) return false;
+  if (combine == C_ADD) {
+    // a+b is NaN only for inf + -inf; -0 only for -0 + -0 (round-to-nearest).
+    if (((fa & S_PINF) && (fb & S_NINF)) || ((fa & S_NINF) && (fb & S_PINF))) return false;
+    if ((fa & S_NZERO) && (fb & S_NZERO)) return false;
+    return true;
+  }
+  if (combine == C_SUB) {
+    // a-b is NaN only for inf - inf of equal sign; -0 only for -0 - +0.
+    if (((fa & S_PINF) && (fb & S_PINF)) || ((fa & S_NINF) && (fb & S_NINF))) return false;
+    if ((fa & S_NZERO) && (fb & S_PZERO)) return false;
+    return true;
+  }
+  return false;
+}
+
+}  // namespace moa

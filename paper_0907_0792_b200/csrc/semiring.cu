@@ -1,0 +1,333 @@
+// K2: the CUDA-core semiring kernel — every (combine, reduce) pair other than
+// the tensor-core (multiply, add) float64 path.
+//
+// Reference loop (_ckernel.pyx:55-72, generic; :37-52 for (multiply, add)):
+//     for i in rows: for l < rowsinred: av = a[l + i*lstride]
+//         for j < elsinop: res[i*restride+j] = reduce(res[..], combine(av, b[l*rstride+j]))
+// Every result element is an l-ascending fold from the identity.  Rows (and
+// elements) are independent, so the GPU tiles C into 128x128 blocks and gives
+// each thread an 8x8 register tile; each thread still folds its elements over
+// l in ascending order with the reference's exact operations, which makes the
+// result bit-identical to the reference for every pair (the "exact" loop).
+//
+// For combine in {add, subtract} with reduce in {min, max} on float32 — the
+// tropical semirings, BASELINE config 5 — the exact loop costs a FADD, FSETP
+// and FSEL per pair.  The fast loop instead adds two contraction steps at once
+// with a packed FADD2 and folds both sums with one 3-input FMNMX3 (about 2.5x
+// the pair rate, tools/peaks.cu).  FMNMX3 prefers non-NaN operands and may
+// order +-0 freely, so it is bit-exact only when no combine result is NaN or
+// -0.0.  A pre-scan kernel records which special values occur in A and B and
+// the main kernel picks the loop on the device (fast_fold_is_exact), so no
+// host synchronisation is needed and the result never depends on the choice.
+//
+// Shared-memory layout: both tiles are stored as k-PAIRS, As[kp][m] =
+// (A[m][2kp], A[m][2kp+1]) and Bs[kp][n] = (B[2kp][n], B[2kp+1][n]), so a
+// thread's FADD2 operands are single 64-bit LDS results.  Thread (ty, tx) owns
+// rows ty*8..ty*8+7 and columns 32g + 2tx + {0,1} (g < 4): A reads are
+// warp-broadcasts, B reads are 16-byte loads over a contiguous 256-byte span
+// (conflict-free).  Global->shared staging is register double-buffered.
+#include "moa_common.cuh"
+#include "moa_kernels.h"
+#include "../../include/moa_b200.h"
+
+namespace moa {
+
+namespace {
+
+constexpr int SBM = 128, SBN = 128, SBK = 16, SKP = SBK / 2, SNT = 256, GROUP_M = 8;
+
+template <typename T> struct alignas(2 * sizeof(T)) KPair { T x, y; };
+
+template <typename T>
+struct SemiringSmem {
+  KPair<T> a[2][SKP][SBM];
+  KPair<T> b[2][SKP][SBN];
+};
+
+// value used for k beyond K in the FAST loop: it must contribute the reduce
+// identity, i.e. combine(pad_a, pad_b) = +inf for min and -inf for max.
+template <typename T, int C, int R> __device__ __forceinline__ T pad_a() {
+  return (R == R_MIN) ? T(__builtin_huge_val()) : T(-__builtin_huge_val());
+}
+template <typename T, int C, int R> __device__ __forceinline__ T pad_b() {
+  // add: (+inf)+(+inf)=+inf, (-inf)+(-inf)=-inf; subtract: (+inf)-(-inf)=+inf, (-inf)-(+inf)=-inf
+  const T v = (R == R_MIN) ? T(__builtin_huge_val()) : T(-__builtin_huge_val());
+  return C == C_SUB ? -v : v;
+}
+
+__device__ __forceinline__ unsigned long long f32x2_bits(KPair<float> p) {
+  return *reinterpret_cast<unsigned long long*>(&p);
+}
+
+// one FADD2: (a.x op b.x, a.y op b.y), round-to-nearest each
+template <int C>
+__device__ __forceinline__ void pair_combine(KPair<float> a, KPair<float> b, float& s0, float& s1) {
+  unsigned long long r;
+  if (C == C_SUB)
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f32x2_bits(a)), "l"(f32x2_bits(b)));
+  else
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f32x2_bits(a)), "l"(f32x2_bits(b)));
+  s0 = __uint_as_float((unsigned)r);
+  s1 = __uint_as_float((unsigned)(r >> 32));
+}
+
+template <int R>
+__device__ __forceinline__ float fold3(float acc, float s0, float s1) {
+  float r;
+  if (R == R_MIN)
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(acc), "f"(s0), "f"(s1));
+  else
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(acc), "f"(s0), "f"(s1));
+  return r;
+}
+
+template <typename T, int C, int R, bool ACC, bool FASTCAND>
+__global__ void __launch_bounds__(SNT) semiring_kernel(T* __restrict__ c, const T* __restrict__ a,
+                                                       const T* __restrict__ b, int64_t M, int64_t N,
+                                                       int64_t K, int64_t lda, int64_t ldb,
+                                                       int64_t ldc, const unsigned* special,
+                                                       int64_t tiles_m, int64_t tiles_n) {
+  using A = typename AccType<T, R>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SemiringSmem<T>& sm = *reinterpret_cast<SemiringSmem<T>*>(smem_raw);
+
+  // grouped rasterisation: GROUP_M row tiles sweep the column tiles together
+  const int64_t pid = blockIdx.x;
+  const int64_t width = GROUP_M * tiles_n;
+  const int64_t first_m = (pid / width) * GROUP_M;
+  const int64_t gsize = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
+  const int64_t tm = first_m + (pid % width) % gsize;
+  const int64_t tn = (pid % width) / gsize;
+  const int64_t m0 = tm * SBM, n0 = tn * SBN;
+
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;
+
+  bool fast = false;
+  if (FASTCAND && !ACC) fast = fast_fold_is_exact(C, __ldg(special), __ldg(special + 1));
+
+  // ---- accumulators ----
+  A acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int64_t row = m0 + ty * 8 + i;
+      const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
+      if (ACC && row < M && col < N)
+        acc[i][j] = A(c[row * ldc + col]);
+      else
+        acc[i][j] = ReduceOp<R>::template identity<A>();
+    }
+
+  // ---- global -> register staging (each thread: 8 A values, 8 B values) ----
+  const int a_row = tid >> 1, a_k = (tid & 1) * 8;    // A: row, first k of 8
+  const int b_k = tid >> 4, b_col = (tid & 15) * 8;   // B: k row, first of 8 columns
+  const T pa = FASTCAND ? pad_a<T, C, R>() : T(0);
+  const T pb = FASTCAND ? pad_b<T, C, R>() : T(0);
+  T ra[8], rb[8];
+  auto load_tile = [&](int64_t k0) {
+    const int64_t gm = m0 + a_row;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int64_t gk = k0 + a_k + q;
+      ra[q] = (gm < M && gk < K) ? __ldg(a + gm * lda + gk) : pa;
+    }
+    const int64_t gk = k0 + b_k;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int64_t gn = n0 + b_col + q;
+      rb[q] = (gk < K && gn < N) ? __ldg(b + gk * ldb + gn) : pb;
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 8; q += 2)
+      sm.a[buf][(a_k + q) >> 1][a_row] = KPair<T>{ra[q], ra[q + 1]};
+    T* bs = reinterpret_cast<T*>(&sm.b[buf][b_k >> 1][0]);
+#pragma unroll
+    for (int q = 0; q < 8; q++) bs[2 * (b_col + q) + (b_k & 1)] = rb[q];
+  };
+
+  const int64_t KT = (K + SBK - 1) / SBK;
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+
+  for (int64_t kt = 0; kt < KT; kt++) {
+    const int cur = (int)(kt & 1);
+    if (kt + 1 < KT) load_tile((kt + 1) * SBK);
+
+    if (FASTCAND && fast) {
+      if constexpr (FASTCAND && sizeof(T) == 4) {
+#pragma unroll 2
+        for (int kp = 0; kp < SKP; kp++) {
+          KPair<float> ap[8], bp[8];
+          const float4* pa4 = reinterpret_cast<const float4*>(&sm.a[cur][kp][ty * 8]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float4 v = pa4[q];
+            ap[2 * q] = KPair<float>{v.x, v.y};
+            ap[2 * q + 1] = KPair<float>{v.z, v.w};
+          }
+#pragma unroll
+          for (int g = 0; g < 4; g++) {
+            const float4 v = *reinterpret_cast<const float4*>(&sm.b[cur][kp][32 * g + 2 * tx]);
+            bp[2 * g] = KPair<float>{v.x, v.y};
+            bp[2 * g + 1] = KPair<float>{v.z, v.w};
+          }
+#pragma unroll
+          for (int i = 0; i < 8; i++)
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              float s0, s1;
+              pair_combine<C>(ap[i], bp[j], s0, s1);
+              acc[i][j] = fold3<R>(acc[i][j], s0, s1);
+            }
+        }
+      }
+    } else {
+      // exact loop: the reference's fold, k ascending, padded k skipped
+      const int64_t krem = K - kt * SBK;
+      const int kend = krem < SBK ? (int)krem : SBK;
+      for (int kk = 0; kk < kend; kk++) {
+        const T* as = reinterpret_cast<const T*>(&sm.a[cur][kk >> 1][ty * 8]) + (kk & 1);
+        const T* bs = reinterpret_cast<const T*>(&sm.b[cur][kk >> 1][2 * tx]) + (kk & 1);
+        A av[8], bv[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) av[i] = A(as[2 * i]);
+#pragma unroll
+        for (int j = 0; j < 8; j++) bv[j] = A(bs[2 * (32 * (j >> 1) + (j & 1))]);
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
+      }
+    }
+    __syncthreads();
+    if (kt + 1 < KT) {
+      store_tile(cur ^ 1);
+      __syncthreads();
+    }
+  }
+
+  // ---- epilogue ----
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int64_t row = m0 + ty * 8 + i;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
+      if (col < N) c[row * ldc + col] = convert<T, A>(acc[i][j]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) scan_special_kernel(const T* __restrict__ x, int64_t rows,
+                                                           int64_t cols, int64_t ld,
+                                                           unsigned* __restrict__ out) {
+  unsigned bits = 0;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const T* p = x + r * ld;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const T v = __ldg(p + j);
+      if (v != v) bits |= S_NAN;
+      else if (v == T(__builtin_huge_val())) bits |= S_PINF;
+      else if (v == T(-__builtin_huge_val())) bits |= S_NINF;
+      else if (v == T(0)) bits |= signbit(v) ? S_NZERO : S_PZERO;
+    }
+  }
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(out, bits);
+}
+
+template <typename T>
+void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* out,
+                 cudaStream_t s) {
+  const unsigned bx = 256;
+  int64_t gx = (cols + bx - 1) / bx;
+  if (gx > 64) gx = 64;
+  int64_t gy = ((int64_t)kNumSMs * 8 + gx - 1) / gx;
+  if (gy > rows) gy = rows;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  scan_special_kernel<T><<<dim3((unsigned)gx, (unsigned)gy), bx, 0, s>>>(x, rows, cols, ld, out);
+  count_launch();
+}
+
+template <typename T, int C, int R, bool ACC, bool FASTCAND>
+cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
+  auto kern = semiring_kernel<T, C, R, ACC, FASTCAND>;
+  const size_t smem = sizeof(SemiringSmem<T>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles_m = (p.M + SBM - 1) / SBM, tiles_n = (p.N + SBN - 1) / SBN;
+  const int64_t tiles = tiles_m * tiles_n;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)tiles, SNT, smem, p.stream>>>(
+      static_cast<T*>(p.c), static_cast<const T*>(p.a), static_cast<const T*>(p.b), p.M, p.N, p.K,
+      p.lda, p.ldb, p.ldc, special, tiles_m, tiles_n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T, int C, int R>
+cudaError_t semiring_acc(const Problem& p) {
+  if (p.accumulate) return semiring_launch<T, C, R, true, false>(p, nullptr);
+  constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB) &&
+                        (R == R_MIN || R == R_MAX);
+  if constexpr (cand) {
+    // pre-scan A (M x K, lda) and B (K x N, ldb) for NaN / +-inf / +-0
+    unsigned* special = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&special), 2 * sizeof(unsigned), p.stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(special, 0, 2 * sizeof(unsigned), p.stream);
+    if (e != cudaSuccess) return e;
+    launch_scan<T>(static_cast<const T*>(p.a), p.M, p.K, p.lda, special, p.stream);
+    launch_scan<T>(static_cast<const T*>(p.b), p.K, p.N, p.ldb, special + 1, p.stream);
+    e = semiring_launch<T, C, R, false, true>(p, special);
+    cudaError_t e2 = cudaFreeAsync(special, p.stream);
+    return e != cudaSuccess ? e : e2;
+  } else {
+    return semiring_launch<T, C, R, false, false>(p, nullptr);
+  }
+}
+
+template <typename T, int C>
+cudaError_t semiring_red(const Problem& p) {
+  switch (p.reduce) {
+    case R_ADD: return semiring_acc<T, C, R_ADD>(p);
+    case R_MUL: return semiring_acc<T, C, R_MUL>(p);
+    case R_MIN: return semiring_acc<T, C, R_MIN>(p);
+    default: return semiring_acc<T, C, R_MAX>(p);
+  }
+}
+
+template <typename T>
+cudaError_t semiring_comb(const Problem& p) {
+  switch (p.combine) {
+    case C_ADD: return semiring_red<T, C_ADD>(p);
+    case C_SUB: return semiring_red<T, C_SUB>(p);
+    case C_MUL: return semiring_red<T, C_MUL>(p);
+    case C_DIV: return semiring_red<T, C_DIV>(p);
+    case C_MIN: return semiring_red<T, C_MIN>(p);
+    default: return semiring_red<T, C_MAX>(p);
+  }
+}
+
+}  // namespace
+
+bool semiring_fast_candidate(int dtype, int combine, int reduce, bool accumulate) {
+  return dtype == MOA_DTYPE_F32 && !accumulate && (combine == C_ADD || combine == C_SUB) &&
+         (reduce == R_MIN || reduce == R_MAX);
+}
+
+cudaError_t launch_semiring(const Problem& p) {
+  return p.dtype == MOA_DTYPE_F64 ? semiring_comb<double>(p) : semiring_comb<float>(p);
+}
+
+}  // namespace moa

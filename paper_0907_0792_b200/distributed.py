@@ -1,0 +1,135 @@
+"""One process per GPU: row-sharded products with one broadcast of B.
+
+This is the multi-GPU form of the reference's fork-join over result rows
+(parallel.py:19-43): rank r of a ``torch.distributed`` group owns the
+contiguous block of result rows ``row_block(noproc, world, r)`` and the
+matching rows of A.  The only exchange the path has is B, which every row
+needs: rank 0 holds it and one ``broadcast`` (NCCL over NVLink/NVSwitch on
+B200, gloo on CPU) gives every rank a copy.  No reduction follows, because
+rows are independent; result blocks stay on their GPU unless ``gather_rows``
+is asked for them.
+
+The per-rank compute is ``row_kernel(plan_block, c_block, a_block, b, ops)``,
+by default the CUDA backend (``kernel.launch``).  The injection point exists
+so the host logic (partitioning, broadcast, gather) can be tested with gloo on
+CPU; it is not a fallback — the default has no CPU path.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+from .kernel import KernelPlan, launch
+from .ops import MUL_ADD, OpPair
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def row_block(noproc: int, world: int, rank: int) -> tuple[int, int]:
+    """[r0, r1) rows owned by ``rank``: ceil-sized contiguous blocks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world size {world}")
+    size = -(-noproc // world) if noproc else 0
+    return min(rank * size, noproc), min((rank + 1) * size, noproc)
+
+
+def block_plan(plan: KernelPlan, r0: int, r1: int) -> KernelPlan:
+    """The plan of rows [r0, r1) of ``plan`` as a stand-alone product."""
+    return KernelPlan(plan.mode, r1 - r0, plan.rowsinred, plan.elsinop, plan.lstride,
+                      plan.rstride, plan.restride, plan.result_shape)
+
+
+def broadcast_operand(b, plan: KernelPlan, *, src: int = 0, group=None, device=None,
+                      dtype=None):
+    """B (rowsinred x elsinop, flat) on every rank; ``b`` is only read on ``src``."""
+    torch, dist = _torch(), _dist()
+    n = plan.rowsinred * plan.elsinop
+    if dist.get_rank(group) == src:
+        buf = b.reshape(-1)
+        if device is not None:
+            buf = buf.to(device)
+        buf = buf.contiguous()
+    else:
+        buf = torch.empty(n, dtype=dtype if dtype is not None else b.dtype,
+                          device=device if device is not None else "cpu")
+    dist.broadcast(buf, src=src, group=group)
+    return buf
+
+
+def _cuda_rows(plan: KernelPlan, c, a, b, ops: OpPair, exact: bool = False) -> None:
+    launch(plan, c, a, b, ops, exact=exact)
+
+
+def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, group=None,
+                    src: int = 0, exact: bool = False, out=None,
+                    row_kernel: Callable | None = None):
+    """This rank's result block of ``plan``.
+
+    a_block: this rank's rows of A (flat, rows row_block(...)), on this rank's
+    device; b: the full B on rank ``src`` (ignored elsewhere).  Returns the flat
+    result block (rows r0..r1 of C) on the same device as a_block.
+    """
+    torch, dist = _torch(), _dist()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    r0, r1 = row_block(plan.noproc, world, rank)
+    sub = block_plan(plan, r0, r1)
+    if a_block.numel() != (r1 - r0) * plan.lstride:
+        raise ValueError(f"rank {rank} owns rows [{r0}, {r1}) = {(r1 - r0) * plan.lstride} "
+                         f"A elements, got {a_block.numel()}")
+    b_all = broadcast_operand(b, plan, src=src, group=group, device=a_block.device,
+                              dtype=a_block.dtype)
+    c = out if out is not None else torch.empty(sub.noproc * sub.elsinop,
+                                                dtype=a_block.dtype, device=a_block.device)
+    if sub.noproc:
+        (row_kernel or (lambda p, c_, a_, b_, o: _cuda_rows(p, c_, a_, b_, o, exact)))(
+            sub, c, a_block, b_all, ops)
+    return c
+
+
+def gather_rows(c_block, plan: KernelPlan, *, dst: int = 0, group=None):
+    """Concatenate every rank's result block on ``dst`` (None elsewhere)."""
+    torch, dist = _torch(), _dist()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    size = -(-plan.noproc // world) if plan.noproc else 0
+    n = plan.elsinop
+    padded = torch.zeros(size * n, dtype=c_block.dtype, device=c_block.device)
+    padded[:c_block.numel()] = c_block
+    if dist.get_backend(group) == "nccl":
+        full = torch.empty(world * size * n, dtype=c_block.dtype, device=c_block.device)
+        dist.all_gather_into_tensor(full, padded, group=group)
+        return full[:plan.noproc * n] if rank == dst else None
+    parts = [torch.empty_like(padded) for _ in range(world)] if rank == dst else None
+    dist.gather(padded, parts, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat(parts)[:plan.noproc * n]
+
+
+def sharded_product_host(plan: KernelPlan, a_block_host, b_host, ops: OpPair = MUL_ADD, *,
+                         device, group=None, src: int = 0, exact: bool = False):
+    """Host-buffer form of ``sharded_product``: copy this rank's A rows (and B on
+    ``src``) to ``device``, broadcast B, compute, and copy the result block back
+    to pinned host memory (returned as a numpy vector)."""
+    torch = _torch()
+    a_dev = _to_device(a_block_host, device)
+    b_dev = _to_device(b_host, device) if b_host is not None else None
+    c = sharded_product(plan, a_dev, b_dev, ops, group=group, src=src, exact=exact)
+    out = torch.empty(c.numel(), dtype=c.dtype, pin_memory=True)
+    out.copy_(c, non_blocking=True)
+    torch.cuda.current_stream(c.device).synchronize()
+    return out.numpy()
+
+
+def _to_device(x, device):
+    torch = _torch()
+    if not isinstance(x, torch.Tensor):
+        x = torch.from_numpy(x)
+    return x.to(device, non_blocking=True)
