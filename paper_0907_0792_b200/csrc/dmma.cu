@@ -11,7 +11,7 @@
 // the warp's register-resident block of C rows.
 //
 // Tiling: CTA tile BM x BN, warp tile WM x WN built from m16n8k4 MMAs (each a
-// DMMA.8x8x4 pair); BK = 16; STAGES-deep cp.async pipeline (LDGSTS, 16-byte
+// DMMA.8x8x4 pair); BK = 16 or 32; STAGES-deep cp.async pipeline (LDGSTS, 16-byte
 // when rows are 16-byte aligned, else 8-byte), OOB elements zero-filled by
 // the copy's src-size so edges need no branches in the main loop.
 // Shared layouts are padded so every fragment LDS.64 is conflict-free:
@@ -29,7 +29,6 @@ namespace moa {
 
 namespace {
 
-constexpr int DBK = 16;
 constexpr int DGROUP_M = 8;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -59,9 +58,10 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int BK_ = 16, int MINB_ = 1>
 struct DmmaCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int DBK = BK_, MIN_BLOCKS = MINB_;
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int MI = WM / 16, NI = WN / 8;
@@ -73,13 +73,13 @@ struct DmmaCfg {
 };
 
 template <class Cfg, bool VEC16, bool ACC>
-__global__ void __launch_bounds__(Cfg::THREADS, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ b,
                 int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                 int64_t tiles_m, int64_t tiles_n) {
   constexpr int BM = Cfg::BM, BN = Cfg::BN, WM = Cfg::WM, WN = Cfg::WN, STAGES = Cfg::STAGES;
   constexpr int MI = Cfg::MI, NI = Cfg::NI, LDA_S = Cfg::LDA_S, LDB_S = Cfg::LDB_S;
-  constexpr int THREADS = Cfg::THREADS;
+  constexpr int THREADS = Cfg::THREADS, DBK = Cfg::DBK;
   extern __shared__ __align__(16) double dsm[];
   double* As = dsm;
   double* Bs = dsm + STAGES * Cfg::A_STAGE;
@@ -219,8 +219,13 @@ cudaError_t dmma_launch(const Problem& p) {
   return cudaGetLastError();
 }
 
-using CfgLarge = DmmaCfg<128, 128, 64, 32, 4>;  // 8 warps, 146 KiB smem, 1 CTA/SM
-using CfgSmall = DmmaCfg<64, 64, 32, 32, 4>;    // 4 warps, 74 KiB smem
+// Tile configurations (tools/tune_dmma.cu sweep, profiles/r01_tune_dmma*.jsonl):
+// large: 64x128 CTA, 8 warps of 32x32, 4 stages, 2 CTAs/SM  -> 88.9% of peak at c4
+// medium: 64x64 CTA, 4 warps of 32x32, 3 stages, 3 CTAs/SM
+// small: 32x32 CTA, 4 warps of 16x16, BK=32 (few k-tile round trips; c1-sized problems)
+using CfgLarge = DmmaCfg<64, 128, 32, 32, 4, 16, 2>;
+using CfgMedium = DmmaCfg<64, 64, 32, 32, 3, 16, 3>;
+using CfgSmall = DmmaCfg<32, 32, 16, 16, 3, 32, 1>;
 
 template <class Cfg>
 cudaError_t dmma_dispatch(const Problem& p) {
@@ -235,9 +240,11 @@ cudaError_t dmma_dispatch(const Problem& p) {
 }  // namespace
 
 cudaError_t launch_dmma(const Problem& p) {
-  // enough 128x128 tiles to fill the 148 SMs at least ~2 waves -> large tiles
-  const int64_t large_tiles = ((p.M + 127) / 128) * ((p.N + 127) / 128);
-  if (large_tiles >= 2 * kNumSMs) return dmma_dispatch<CfgLarge>(p);
+  // all configurations give identical bits (k order is fixed), so the choice
+  // only has to fill the 148 SMs
+  auto tiles = [&](int bm, int bn) { return ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn); };
+  if (tiles(64, 128) >= 2 * kNumSMs) return dmma_dispatch<CfgLarge>(p);
+  if (tiles(64, 64) >= kNumSMs) return dmma_dispatch<CfgMedium>(p);
   return dmma_dispatch<CfgSmall>(p);
 }
 

@@ -87,7 +87,8 @@ template <> __device__ __forceinline__ float convert<float, double>(double x) { 
 // operand special-value flags from the device pre-scan (semiring fast path)
 // ---------------------------------------------------------------------------
 enum SpecialBits : unsigned {
-  S_NAN = 1u, S_PINF = 2u, S_NINF = 4u, S_NZERO = 8u, S_PZERO = 16u
+  S_NAN = 1u, S_PINF = 2u, S_NINF = 4u, S_NZERO = 8u, S_PZERO = 16u,
+  S_NEG = 32u  // sign bit set (any negative value, -0.0 or -inf)
 };
 
 // Whether a fold with the hardware 3-input min/max (FMNMX3, which prefers the
@@ -111,6 +112,18 @@ __host__ __device__ inline bool fast_fold_is_exact(int combine, unsigned fa, uns
     return true;
   }
   return false;
+}
+
+// Fold mode for the float32 tropical loops: 0 = exact compare-select,
+// 1 = FMNMX3 on floats, 2 = VIMNMX3 on the bit patterns.  Mode 2 needs every
+// combine result to be a non-negative, non-NaN float, for which unsigned
+// integer order equals float order (and +-0 ties cannot occur): true for
+// add of two sign-clear, NaN-free operands.  VIMNMX3 issues faster beside
+// FADD2 than FMNMX3 does (profiles/r01_minplus_mix2.json).
+__host__ __device__ inline int tropical_fold_mode(int combine, unsigned fa, unsigned fb) {
+  if (!fast_fold_is_exact(combine, fa, fb)) return 0;
+  if (combine == C_ADD && !((fa | fb) & (S_NAN | S_NEG))) return 2;
+  return 1;
 }
 
 }  // namespace moa

@@ -26,6 +26,8 @@
 // rows ty*8..ty*8+7 and columns 32g + 2tx + {0,1} (g < 4): A reads are
 // warp-broadcasts, B reads are 16-byte loads over a contiguous 256-byte span
 // (conflict-free).  Global->shared staging is register double-buffered.
+#include <type_traits>
+
 #include "moa_common.cuh"
 #include "moa_kernels.h"
 #include "../../include/moa_b200.h"
@@ -38,21 +40,29 @@ constexpr int SBM = 128, SBN = 128, SBK = 16, SKP = SBK / 2, SNT = 256, GROUP_M 
 
 template <typename T> struct alignas(2 * sizeof(T)) KPair { T x, y; };
 
-template <typename T>
-struct SemiringSmem {
-  KPair<T> a[2][SKP][SBM];
-  KPair<T> b[2][SKP][SBN];
+// float32 min/max tiles keep 64 float accumulators and run two CTAs per SM
+// (16 warps); float64 or float64-accumulated tiles need twice the registers.
+template <typename T, int R> struct SemiringShape {
+  static constexpr int STAGES = sizeof(typename AccType<T, R>::type) == 4 ? 4 : 3;
+  static constexpr int MIN_BLOCKS = sizeof(typename AccType<T, R>::type) == 4 ? 2 : 1;
+  static constexpr int A_STAGE = SKP * SBM;  // pairs
+  static constexpr int B_STAGE = SKP * SBN;  // pairs
+  static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(KPair<T>);
 };
 
-// value used for k beyond K in the FAST loop: it must contribute the reduce
-// identity, i.e. combine(pad_a, pad_b) = +inf for min and -inf for max.
-template <typename T, int C, int R> __device__ __forceinline__ T pad_a() {
-  return (R == R_MIN) ? T(__builtin_huge_val()) : T(-__builtin_huge_val());
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-template <typename T, int C, int R> __device__ __forceinline__ T pad_b() {
-  // add: (+inf)+(+inf)=+inf, (-inf)+(-inf)=-inf; subtract: (+inf)-(-inf)=+inf, (-inf)-(+inf)=-inf
-  const T v = (R == R_MIN) ? T(__builtin_huge_val()) : T(-__builtin_huge_val());
-  return C == C_SUB ? -v : v;
+template <int BYTES>
+__device__ __forceinline__ void cp_async_elem(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(dst)), "l"(src),
+               "n"(BYTES), "r"(valid ? BYTES : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long f32x2_bits(KPair<float> p) {
@@ -71,8 +81,12 @@ __device__ __forceinline__ void pair_combine(KPair<float> a, KPair<float> b, flo
   s1 = __uint_as_float((unsigned)(r >> 32));
 }
 
-template <int R>
+template <int R, bool INTFOLD>
 __device__ __forceinline__ float fold3(float acc, float s0, float s1) {
+  if (INTFOLD) {  // non-negative floats: unsigned order == float order
+    const unsigned x = __float_as_uint(acc), y = __float_as_uint(s0), z = __float_as_uint(s1);
+    return __uint_as_float(R == R_MIN ? __vimin3_u32(x, y, z) : __vimax3_u32(x, y, z));
+  }
   float r;
   if (R == R_MIN)
     asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(acc), "f"(s0), "f"(s1));
@@ -82,31 +96,32 @@ __device__ __forceinline__ float fold3(float acc, float s0, float s1) {
 }
 
 template <typename T, int C, int R, bool ACC, bool FASTCAND>
-__global__ void __launch_bounds__(SNT) semiring_kernel(T* __restrict__ c, const T* __restrict__ a,
-                                                       const T* __restrict__ b, int64_t M, int64_t N,
-                                                       int64_t K, int64_t lda, int64_t ldb,
-                                                       int64_t ldc, const unsigned* special,
-                                                       int64_t tiles_m, int64_t tiles_n) {
+__global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
+    semiring_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ b,
+                    int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                    const unsigned* special, int64_t tiles_m, int64_t tiles_n) {
   using A = typename AccType<T, R>::type;
+  using Shape = SemiringShape<T, R>;
+  constexpr int STAGES = Shape::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SemiringSmem<T>& sm = *reinterpret_cast<SemiringSmem<T>*>(smem_raw);
+  KPair<T>* As = reinterpret_cast<KPair<T>*>(smem_raw);
+  KPair<T>* Bs = As + STAGES * Shape::A_STAGE;
 
   // grouped rasterisation: GROUP_M row tiles sweep the column tiles together
   const int64_t pid = blockIdx.x;
   const int64_t width = GROUP_M * tiles_n;
   const int64_t first_m = (pid / width) * GROUP_M;
   const int64_t gsize = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
-  const int64_t tm = first_m + (pid % width) % gsize;
-  const int64_t tn = (pid % width) / gsize;
-  const int64_t m0 = tm * SBM, n0 = tn * SBN;
+  const int64_t m0 = (first_m + (pid % width) % gsize) * SBM;
+  const int64_t n0 = ((pid % width) / gsize) * SBN;
 
   const int tid = threadIdx.x;
   const int ty = tid >> 4, tx = tid & 15;
 
-  bool fast = false;
-  if (FASTCAND && !ACC) fast = fast_fold_is_exact(C, __ldg(special), __ldg(special + 1));
+  int mode = 0;  // 0 exact, 1 FMNMX3, 2 VIMNMX3 (see tropical_fold_mode)
+  if (FASTCAND && !ACC) mode = tropical_fold_mode(C, __ldg(special), __ldg(special + 1));
 
-  // ---- accumulators ----
+  // ---- accumulators: rows ty*8+i, columns 32*(j>>1) + 2*tx + (j&1) ----
   A acc[8][8];
 #pragma unroll
   for (int i = 0; i < 8; i++)
@@ -120,84 +135,111 @@ __global__ void __launch_bounds__(SNT) semiring_kernel(T* __restrict__ c, const 
         acc[i][j] = ReduceOp<R>::template identity<A>();
     }
 
-  // ---- global -> register staging (each thread: 8 A values, 8 B values) ----
-  const int a_row = tid >> 1, a_k = (tid & 1) * 8;    // A: row, first k of 8
-  const int b_k = tid >> 4, b_col = (tid & 15) * 8;   // B: k row, first of 8 columns
-  const T pa = FASTCAND ? pad_a<T, C, R>() : T(0);
-  const T pb = FASTCAND ? pad_b<T, C, R>() : T(0);
-  T ra[8], rb[8];
-  auto load_tile = [&](int64_t k0) {
-    const int64_t gm = m0 + a_row;
+  // ---- element-wise async copies into the k-pair layouts (zero-filled outside) ----
+  auto load_stage = [&](int stage, int64_t k0) {
+    T* as = reinterpret_cast<T*>(As + stage * Shape::A_STAGE);
+    T* bs = reinterpret_cast<T*>(Bs + stage * Shape::B_STAGE);
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const int64_t gk = k0 + a_k + q;
-      ra[q] = (gm < M && gk < K) ? __ldg(a + gm * lda + gk) : pa;
+    for (int q = 0; q < SBM * SBK / SNT; q++) {
+      const int e = tid + q * SNT;
+      const int r = e / SBK, kk = e % SBK;          // 16 threads read one A row segment
+      const int64_t gm = m0 + r, gk = k0 + kk;
+      const bool ok = gm < M && gk < K;
+      cp_async_elem<sizeof(T)>(as + 2 * ((kk >> 1) * SBM + r) + (kk & 1),
+                               ok ? a + gm * lda + gk : a, ok);
     }
-    const int64_t gk = k0 + b_k;
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const int64_t gn = n0 + b_col + q;
-      rb[q] = (gk < K && gn < N) ? __ldg(b + gk * ldb + gn) : pb;
+    for (int q = 0; q < SBK * SBN / SNT; q++) {
+      const int e = tid + q * SNT;
+      const int kk = e / SBN, n = e % SBN;          // a warp reads 32 consecutive B columns
+      const int64_t gk = k0 + kk, gn = n0 + n;
+      const bool ok = gk < K && gn < N;
+      cp_async_elem<sizeof(T)>(bs + 2 * ((kk >> 1) * SBN + n) + (kk & 1),
+                               ok ? b + gk * ldb + gn : b, ok);
     }
-  };
-  auto store_tile = [&](int buf) {
-#pragma unroll
-    for (int q = 0; q < 8; q += 2)
-      sm.a[buf][(a_k + q) >> 1][a_row] = KPair<T>{ra[q], ra[q + 1]};
-    T* bs = reinterpret_cast<T*>(&sm.b[buf][b_k >> 1][0]);
-#pragma unroll
-    for (int q = 0; q < 8; q++) bs[2 * (b_col + q) + (b_k & 1)] = rb[q];
   };
 
   const int64_t KT = (K + SBK - 1) / SBK;
-  load_tile(0);
-  store_tile(0);
-  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; s++) {
+    if (s < KT) load_stage(s, (int64_t)s * SBK);
+    cp_async_commit();
+  }
 
   for (int64_t kt = 0; kt < KT; kt++) {
-    const int cur = (int)(kt & 1);
-    if (kt + 1 < KT) load_tile((kt + 1) * SBK);
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t nk = kt + STAGES - 1;
+      if (nk < KT) load_stage((int)(nk % STAGES), nk * SBK);
+      cp_async_commit();
+    }
+    const KPair<T>* as = As + (int)(kt % STAGES) * Shape::A_STAGE;
+    const KPair<T>* bs = Bs + (int)(kt % STAGES) * Shape::B_STAGE;
+    const int64_t krem = K - kt * SBK;
+    const int kend = krem < SBK ? (int)krem : SBK;
 
-    if (FASTCAND && fast) {
+    if (FASTCAND && mode != 0) {
       if constexpr (FASTCAND && sizeof(T) == 4) {
-#pragma unroll 2
-        for (int kp = 0; kp < SKP; kp++) {
-          KPair<float> ap[8], bp[8];
-          const float4* pa4 = reinterpret_cast<const float4*>(&sm.a[cur][kp][ty * 8]);
+        auto fast_tile = [&](auto intfold) {
+          constexpr bool INTFOLD = decltype(intfold)::value;
+          auto fast_pair = [&](int kp) {
+            KPair<float> ap[8], bp[8];
+            const float4* pa4 = reinterpret_cast<const float4*>(as + kp * SBM + ty * 8);
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const float4 v = pa4[q];
-            ap[2 * q] = KPair<float>{v.x, v.y};
-            ap[2 * q + 1] = KPair<float>{v.z, v.w};
-          }
-#pragma unroll
-          for (int g = 0; g < 4; g++) {
-            const float4 v = *reinterpret_cast<const float4*>(&sm.b[cur][kp][32 * g + 2 * tx]);
-            bp[2 * g] = KPair<float>{v.x, v.y};
-            bp[2 * g + 1] = KPair<float>{v.z, v.w};
-          }
-#pragma unroll
-          for (int i = 0; i < 8; i++)
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-              float s0, s1;
-              pair_combine<C>(ap[i], bp[j], s0, s1);
-              acc[i][j] = fold3<R>(acc[i][j], s0, s1);
+            for (int q = 0; q < 4; q++) {
+              const float4 v = pa4[q];
+              ap[2 * q] = KPair<float>{v.x, v.y};
+              ap[2 * q + 1] = KPair<float>{v.z, v.w};
             }
-        }
+#pragma unroll
+            for (int g = 0; g < 4; g++) {
+              const float4 v = *reinterpret_cast<const float4*>(bs + kp * SBN + 32 * g + 2 * tx);
+              bp[2 * g] = KPair<float>{v.x, v.y};
+              bp[2 * g + 1] = KPair<float>{v.z, v.w};
+            }
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+              for (int j = 0; j < 8; j++) {
+                float s0, s1;
+                pair_combine<C>(ap[i], bp[j], s0, s1);
+                acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
+              }
+          };
+          if (kend == SBK) {
+#pragma unroll
+            for (int kp = 0; kp < SKP; kp++) fast_pair(kp);
+          } else {
+            for (int kp = 0; kp < kend / 2; kp++) fast_pair(kp);
+            if (kend & 1) {  // lone last k: one scalar combine + 2-input min/max
+              const int kp = kend / 2;
+              float av[8], bv[8];
+#pragma unroll
+              for (int i = 0; i < 8; i++) av[i] = as[kp * SBM + ty * 8 + i].x;
+#pragma unroll
+              for (int j = 0; j < 8; j++) bv[j] = bs[kp * SBN + 32 * (j >> 1) + 2 * tx + (j & 1)].x;
+#pragma unroll
+              for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 8; j++)
+                  acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
+            }
+          }
+        };
+        if (C == C_ADD && mode == 2) fast_tile(std::true_type{});
+        else fast_tile(std::false_type{});
       }
     } else {
-      // exact loop: the reference's fold, k ascending, padded k skipped
-      const int64_t krem = K - kt * SBK;
-      const int kend = krem < SBK ? (int)krem : SBK;
+      // exact loop: the reference's fold, k ascending, k beyond K skipped
       for (int kk = 0; kk < kend; kk++) {
-        const T* as = reinterpret_cast<const T*>(&sm.a[cur][kk >> 1][ty * 8]) + (kk & 1);
-        const T* bs = reinterpret_cast<const T*>(&sm.b[cur][kk >> 1][2 * tx]) + (kk & 1);
+        const T* ak = reinterpret_cast<const T*>(as + (kk >> 1) * SBM + ty * 8) + (kk & 1);
+        const T* bk = reinterpret_cast<const T*>(bs + (kk >> 1) * SBN + 2 * tx) + (kk & 1);
         A av[8], bv[8];
 #pragma unroll
-        for (int i = 0; i < 8; i++) av[i] = A(as[2 * i]);
+        for (int i = 0; i < 8; i++) av[i] = A(ak[2 * i]);
 #pragma unroll
-        for (int j = 0; j < 8; j++) bv[j] = A(bs[2 * (32 * (j >> 1) + (j & 1))]);
+        for (int j = 0; j < 8; j++) bv[j] = A(bk[2 * (32 * (j >> 1) + (j & 1))]);
 #pragma unroll
         for (int i = 0; i < 8; i++)
 #pragma unroll
@@ -205,12 +247,8 @@ __global__ void __launch_bounds__(SNT) semiring_kernel(T* __restrict__ c, const 
             acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
       }
     }
-    __syncthreads();
-    if (kt + 1 < KT) {
-      store_tile(cur ^ 1);
-      __syncthreads();
-    }
   }
+  cp_async_wait<0>();
 
   // ---- epilogue ----
 #pragma unroll
@@ -239,6 +277,7 @@ __global__ void __launch_bounds__(256) scan_special_kernel(const T* __restrict__
       else if (v == T(__builtin_huge_val())) bits |= S_PINF;
       else if (v == T(-__builtin_huge_val())) bits |= S_NINF;
       else if (v == T(0)) bits |= signbit(v) ? S_NZERO : S_PZERO;
+      if (signbit(v)) bits |= S_NEG;
     }
   }
   bits = __reduce_or_sync(0xffffffffu, bits);
@@ -262,7 +301,7 @@ void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* o
 template <typename T, int C, int R, bool ACC, bool FASTCAND>
 cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
   auto kern = semiring_kernel<T, C, R, ACC, FASTCAND>;
-  const size_t smem = sizeof(SemiringSmem<T>);
+  const size_t smem = SemiringShape<T, R>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + SBM - 1) / SBM, tiles_n = (p.N + SBN - 1) / SBN;

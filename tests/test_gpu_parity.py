@@ -279,7 +279,7 @@ def test_dmma_tile_configs_bitwise_identical(rng):
     ad, bd = _dev(a), _dev(b)
     full = torch.empty(m * n, dtype=torch.float64, device="cuda")
     launch(plan_inner((m, k), (k, n)), full, ad, bd, moa.MUL_ADD)
-    for r0, r1 in ((0, 64), (1000, 1130), (4000, 4096)):
+    for r0, r1 in ((0, 64), (1000, 1130), (1000, 1400), (4000, 4096)):  # small, small, medium, small
         sub = torch.empty((r1 - r0) * n, dtype=torch.float64, device="cuda")
         launch(plan_inner((r1 - r0, k), (k, n)), sub, ad[r0 * k:r1 * k], bd, moa.MUL_ADD)
         assert_bits_equal(sub.cpu().numpy(), full[r0 * n:r1 * n].cpu().numpy())
