@@ -78,10 +78,19 @@ def fp64_peak() -> tuple[float, str]:
 
 
 def minplus_peak() -> tuple[float, str]:
-    mb = microbench_peaks()
-    vals = [v for k, v in mb.items() if k.startswith("minplus_fadd2_fmnmx3")]
-    v = max(vals) if vals else 21.13
-    return v * 1000.0, "measured FADD2+FMNMX3 microbenchmark, G pairs/s (profiles/r01_peaks_microbench.json)"
+    """Best measured (add, min) pair rate on the ALU/FMA pipes, G pairs/s.
+
+    profiles/r01_minplus_mix2.json holds warp-instructions per clock per SM for
+    FADD2 + FMNMX3 and FADD2 + VIMNMX3 units (64 pairs each) at 1965 MHz."""
+    p = REPO / "profiles" / "r01_minplus_mix2.json"
+    if p.exists():
+        mix = json.loads(p.read_text())
+        units = max(mix.get("fadd2_fmnmx3_pairs_winstr_per_clk_sm", 0.0),
+                    mix.get("fadd2_vimnmx3_units_winstr_per_clk_sm", 0.0))
+        return (units * 64 * 148 * 1.965e9 / 1e9,
+                "measured FADD2+VIMNMX3 / FADD2+FMNMX3 instruction-mix microbenchmark "
+                "(profiles/r01_minplus_mix2.json), best mix, 1965 MHz")
+    return 24470.0, "measured FADD2+VIMNMX3 microbenchmark (r01)"
 
 
 def ncu_traffic(workload: str):

@@ -36,18 +36,26 @@ namespace moa {
 
 namespace {
 
-constexpr int SBM = 128, SBN = 128, SBK = 16, SKP = SBK / 2, SNT = 256, GROUP_M = 8;
+constexpr int SBM = 128, SBN = 128, SNT = 256, GROUP_M = 8;
 
 template <typename T> struct alignas(2 * sizeof(T)) KPair { T x, y; };
 
 // float32 min/max tiles keep 64 float accumulators and run two CTAs per SM
 // (16 warps); float64 or float64-accumulated tiles need twice the registers.
 template <typename T, int R> struct SemiringShape {
-  static constexpr int STAGES = sizeof(typename AccType<T, R>::type) == 4 ? 4 : 3;
-  static constexpr int MIN_BLOCKS = sizeof(typename AccType<T, R>::type) == 4 ? 2 : 1;
-  static constexpr int A_STAGE = SKP * SBM;  // pairs
-  static constexpr int B_STAGE = SKP * SBN;  // pairs
+  static constexpr bool F4 = sizeof(typename AccType<T, R>::type) == 4;
+  static constexpr int BK = F4 ? 32 : 16;       // k per stage (one barrier per BK)
+  static constexpr int KP = BK / 2;             // k-pairs per stage
+  static constexpr int STAGES = 3;
+  static constexpr int MIN_BLOCKS = F4 ? 2 : 1;
+  static constexpr int A_STAGE = KP * SBM;      // pairs
+  static constexpr int B_STAGE = KP * SBN;      // pairs
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(KPair<T>);
+  // element-wise loader: thread t copies A elements (row t/BK + (SNT/BK)*q, k t%BK)
+  // and B elements (k t/SBN + (SNT/SBN)*q, column t%SBN)
+  static constexpr int QA = SBM * BK / SNT, A_RSTEP = SNT / BK;
+  static constexpr int QB = BK * SBN / SNT, B_KSTEP = SNT / SBN;
+  static_assert(QA <= 32 && B_KSTEP == 2, "loader layout");
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -95,7 +103,14 @@ __device__ __forceinline__ float fold3(float acc, float s0, float s1) {
   return r;
 }
 
-template <typename T, int C, int R, bool ACC, bool FASTCAND>
+#ifndef MOA_SEMIRING_LOOP
+#define MOA_SEMIRING_LOOP 0
+#endif
+
+// LOOP selects the instruction order of the fast loop's 8x8 tile (tuning):
+// 0: element by element; 1: per row, 8 FADD2 then 8 folds; 2: column-major;
+// 3: per row, two batches of 4 FADD2 + 4 folds.  All orders give the same bits.
+template <typename T, int C, int R, bool ACC, bool FASTCAND, int LOOP = MOA_SEMIRING_LOOP>
 __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
     semiring_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ b,
                     int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
@@ -134,35 +149,54 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
       else
         acc[i][j] = ReduceOp<R>::template identity<A>();
     }
+  // The unsigned-order fold (mode 2) cannot start from -inf (sign bit set).
+  // Mode 2 implies every combine result is >= +0 and K >= 2, so a max fold
+  // from +0 gives the same bits as one from the identity.
+  if (FASTCAND && R == R_MAX && mode == 2) {
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+      for (int j = 0; j < 8; j++) acc[i][j] = A(0);
+  }
 
   // ---- element-wise async copies into the k-pair layouts (zero-filled outside) ----
+  // Per-thread bases are fixed for the whole kernel; a stage only adds k0.
+  constexpr int BK = Shape::BK, KP = Shape::KP;
+  const int a_kk = tid % BK, a_r = tid / BK;
+  const int b_n = tid % SBN, b_kk = tid / SBN;
+  const T* a_src = a + (m0 + a_r) * lda + a_kk;
+  const int64_t a_qstep = (int64_t)Shape::A_RSTEP * lda;
+  const T* b_src = b + (int64_t)b_kk * ldb + n0 + b_n;
+  const int64_t b_qstep = (int64_t)Shape::B_KSTEP * ldb;
+  unsigned a_rows_ok = 0;
+#pragma unroll
+  for (int q = 0; q < Shape::QA; q++)
+    if (m0 + a_r + q * Shape::A_RSTEP < M) a_rows_ok |= 1u << q;
+  const bool b_col_ok = n0 + b_n < N;
+  const int a_dst = 2 * ((a_kk >> 1) * SBM + a_r) + (a_kk & 1);   // in T elements
+  const int b_dst = 2 * b_n + b_kk;                                // in T elements
   auto load_stage = [&](int stage, int64_t k0) {
-    T* as = reinterpret_cast<T*>(As + stage * Shape::A_STAGE);
-    T* bs = reinterpret_cast<T*>(Bs + stage * Shape::B_STAGE);
+    T* as = reinterpret_cast<T*>(As + stage * Shape::A_STAGE) + a_dst;
+    T* bs = reinterpret_cast<T*>(Bs + stage * Shape::B_STAGE) + b_dst;
+    const bool a_k_ok = k0 + a_kk < K;
+    const T* pa = a_src + k0;
 #pragma unroll
-    for (int q = 0; q < SBM * SBK / SNT; q++) {
-      const int e = tid + q * SNT;
-      const int r = e / SBK, kk = e % SBK;          // 16 threads read one A row segment
-      const int64_t gm = m0 + r, gk = k0 + kk;
-      const bool ok = gm < M && gk < K;
-      cp_async_elem<sizeof(T)>(as + 2 * ((kk >> 1) * SBM + r) + (kk & 1),
-                               ok ? a + gm * lda + gk : a, ok);
+    for (int q = 0; q < Shape::QA; q++) {
+      const bool ok = a_k_ok && ((a_rows_ok >> q) & 1u);
+      cp_async_elem<sizeof(T)>(as + 2 * Shape::A_RSTEP * q, ok ? pa + q * a_qstep : a, ok);
     }
+    const T* pb = b_src + k0 * ldb;
 #pragma unroll
-    for (int q = 0; q < SBK * SBN / SNT; q++) {
-      const int e = tid + q * SNT;
-      const int kk = e / SBN, n = e % SBN;          // a warp reads 32 consecutive B columns
-      const int64_t gk = k0 + kk, gn = n0 + n;
-      const bool ok = gk < K && gn < N;
-      cp_async_elem<sizeof(T)>(bs + 2 * ((kk >> 1) * SBN + n) + (kk & 1),
-                               ok ? b + gk * ldb + gn : b, ok);
+    for (int q = 0; q < Shape::QB; q++) {
+      const bool ok = b_col_ok && (k0 + b_kk + Shape::B_KSTEP * q < K);
+      cp_async_elem<sizeof(T)>(bs + 2 * SBN * q, ok ? pb + q * b_qstep : b, ok);
     }
   };
 
-  const int64_t KT = (K + SBK - 1) / SBK;
+  const int64_t KT = (K + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; s++) {
-    if (s < KT) load_stage(s, (int64_t)s * SBK);
+    if (s < KT) load_stage(s, (int64_t)s * BK);
     cp_async_commit();
   }
 
@@ -171,13 +205,13 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
     __syncthreads();
     {
       const int64_t nk = kt + STAGES - 1;
-      if (nk < KT) load_stage((int)(nk % STAGES), nk * SBK);
+      if (nk < KT) load_stage((int)(nk % STAGES), nk * BK);
       cp_async_commit();
     }
     const KPair<T>* as = As + (int)(kt % STAGES) * Shape::A_STAGE;
     const KPair<T>* bs = Bs + (int)(kt % STAGES) * Shape::B_STAGE;
-    const int64_t krem = K - kt * SBK;
-    const int kend = krem < SBK ? (int)krem : SBK;
+    const int64_t krem = K - kt * BK;
+    const int kend = krem < BK ? (int)krem : BK;
 
     if (FASTCAND && mode != 0) {
       if constexpr (FASTCAND && sizeof(T) == 4) {
@@ -198,18 +232,42 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
               bp[2 * g] = KPair<float>{v.x, v.y};
               bp[2 * g + 1] = KPair<float>{v.z, v.w};
             }
+            if constexpr (LOOP == 0) {
 #pragma unroll
-            for (int i = 0; i < 8; i++)
+              for (int i = 0; i < 8; i++)
 #pragma unroll
-              for (int j = 0; j < 8; j++) {
-                float s0, s1;
-                pair_combine<C>(ap[i], bp[j], s0, s1);
-                acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
-              }
+                for (int j = 0; j < 8; j++) {
+                  float s0, s1;
+                  pair_combine<C>(ap[i], bp[j], s0, s1);
+                  acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
+                }
+            } else if constexpr (LOOP == 2) {
+#pragma unroll
+              for (int j = 0; j < 8; j++)
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                  float s0, s1;
+                  pair_combine<C>(ap[i], bp[j], s0, s1);
+                  acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
+                }
+            } else {
+              constexpr int BATCH = LOOP == 1 ? 8 : 4;
+#pragma unroll
+              for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j0 = 0; j0 < 8; j0 += BATCH) {
+                  float s0[BATCH], s1[BATCH];
+#pragma unroll
+                  for (int j = 0; j < BATCH; j++) pair_combine<C>(ap[i], bp[j0 + j], s0[j], s1[j]);
+#pragma unroll
+                  for (int j = 0; j < BATCH; j++)
+                    acc[i][j0 + j] = fold3<R, INTFOLD>(acc[i][j0 + j], s0[j], s1[j]);
+                }
+            }
           };
-          if (kend == SBK) {
+          if (kend == BK) {
 #pragma unroll
-            for (int kp = 0; kp < SKP; kp++) fast_pair(kp);
+            for (int kp = 0; kp < KP; kp++) fast_pair(kp);
           } else {
             for (int kp = 0; kp < kend / 2; kp++) fast_pair(kp);
             if (kend & 1) {  // lone last k: one scalar combine + 2-input min/max
@@ -298,9 +356,9 @@ void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* o
   count_launch();
 }
 
-template <typename T, int C, int R, bool ACC, bool FASTCAND>
+template <typename T, int C, int R, bool ACC, bool FASTCAND, int LOOP = MOA_SEMIRING_LOOP>
 cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
-  auto kern = semiring_kernel<T, C, R, ACC, FASTCAND>;
+  auto kern = semiring_kernel<T, C, R, ACC, FASTCAND, LOOP>;
   const size_t smem = SemiringShape<T, R>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -217,7 +217,95 @@ class _Runner:
 
 def execute_sequential(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair = MUL_ADD,
                        *, backend: str | None = None, exact: bool = False) -> MoaArray:
-    """Run the planned product over all result rows in one launch."""
+    """Run the planned product over all result rows.
+
+    Device operands: one launch.  Host operands of a large product: the rows
+    are streamed in blocks (``_stream_chunks``) so the copy of A's next block
+    and of C's previous block overlap the kernel; the bits are those of one
+    launch because rows are independent.
+    """
+    if not (a.is_device or b.is_device):
+        chunks = _stream_chunks(plan, result_dtype(a, b), ops)
+        if chunks > 1:
+            _check_plan(plan, a, b)
+            resolve_backend(backend, ops)
+            return _execute_streamed(plan, a, b, ops, chunks, exact=exact)
     runner = _Runner(plan, a, b, ops, backend, exact=exact)
     runner.run_rows(0, 1)
     return runner.finish()
+
+
+_STREAM_MIN_OUT_BYTES = 128 << 20
+_WAVES_PER_CHUNK = 24  # >= 24 waves of CTAs per block keeps the tail wave small
+
+
+def _stream_chunks(plan: KernelPlan, dtype: np.dtype, ops: OpPair = MUL_ADD) -> int:
+    """Row blocks for the streamed host path (1 = do not stream)."""
+    if plan.rowsinred < 2:  # outer products are pure D2H; blocks cannot hide it
+        return 1
+    out_bytes = plan.noproc * plan.elsinop * np.dtype(dtype).itemsize
+    if ops.codes() == (2, 0) and np.dtype(dtype) == np.dtype(np.float64):
+        tiles, per_wave = -(-plan.noproc // 64) * -(-plan.elsinop // 128), 296  # dmma.cu
+    else:
+        tiles, per_wave = -(-plan.noproc // 128) * -(-plan.elsinop // 128), 296  # semiring.cu
+    by_waves = tiles // (per_wave * _WAVES_PER_CHUNK)
+    return int(max(1, min(8, out_bytes // _STREAM_MIN_OUT_BYTES, by_waves)))
+
+
+def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, chunks: int,
+                      *, exact: bool = False, device=None) -> MoaArray:
+    """Host operands -> host result with copies overlapped with compute.
+
+    B goes to the device first (every row needs it); then for each row block:
+    H2D of its A rows on a copy stream, the kernel on the compute stream, D2H
+    of its C rows on a second copy stream, with two-deep device buffers.
+    """
+    from .parallel import row_blocks  # local: parallel imports this module
+    torch = _torch()
+    _native.load()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else \
+        torch.device(device)
+    dtype = result_dtype(a, b)
+    tdt = torch.float32 if dtype == np.dtype(np.float32) else torch.float64
+    m, n, lda = plan.noproc, plan.elsinop, plan.lstride
+    comp = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    b_dev = stage(b, dev, dtype)
+    out = torch.empty(m * n, dtype=tdt, pin_memory=True)
+    blocks = [r for r in row_blocks(m, chunks) if len(r)]
+    rows_max = max(len(r) for r in blocks)
+    a_buf = [torch.empty(rows_max * lda, dtype=tdt, device=dev) for _ in range(2)]
+    c_buf = [torch.empty(rows_max * n, dtype=tdt, device=dev) for _ in range(2)]
+    a_free = [None, None]
+    c_free = [None, None]
+    host_a = a.data if a.data.dtype == dtype else a.data.astype(dtype)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        host_a_t = torch.from_numpy(host_a)
+    for idx, rows in enumerate(blocks):
+        slot, r0, r1 = idx % 2, rows.start, rows.stop
+        na, nc = (r1 - r0) * lda, (r1 - r0) * n
+        with torch.cuda.stream(s_in):
+            if a_free[slot] is not None:
+                s_in.wait_event(a_free[slot])
+            a_buf[slot][:na].copy_(host_a_t[r0 * lda:r1 * lda], non_blocking=True)
+            a_ready = torch.cuda.Event()
+            a_ready.record(s_in)
+        comp.wait_event(a_ready)
+        if c_free[slot] is not None:
+            comp.wait_event(c_free[slot])
+        sub = KernelPlan(plan.mode, r1 - r0, plan.rowsinred, n, lda, plan.rstride, plan.restride,
+                         plan.result_shape)
+        launch(sub, c_buf[slot][:nc], a_buf[slot][:na], b_dev, ops, exact=exact, stream=comp)
+        done = torch.cuda.Event()
+        done.record(comp)
+        a_free[slot] = done
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(done)
+            out[r0 * n:r1 * n].copy_(c_buf[slot][:nc], non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(s_out)
+            c_free[slot] = copied
+    s_out.synchronize()
+    comp.synchronize()
+    return MoaArray._wrap(plan.result_shape, out.numpy())

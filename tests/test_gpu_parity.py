@@ -290,7 +290,7 @@ def test_dmma_tile_configs_bitwise_identical(rng):
 def test_tropical_fast_and_exact_loops_agree(rng):
     """float32 (add|subtract, min|max): the FMNMX3 loop (clean data) and the
     compare-select loop (data with NaN/-0) both equal the reference."""
-    m, k, n = 257, 130, 300
+    m, k, n = 257, 131, 300  # odd K: the last k of the last tile takes the scalar tail
     for comb in ("add", "subtract"):
         for red in ("min", "max"):
             ops = op_pair(comb, red)
@@ -299,9 +299,11 @@ def test_tropical_fast_and_exact_loops_agree(rng):
             b = rng.random(k * n, dtype=np.float32) * np.float32(100)
             a[rng.random(m * k) < 0.05] = np.inf
             b[rng.random(k * n) < 0.05] = np.inf if comb == "add" else -np.inf
-            for poison in (None, "nan", "negzero"):
+            for poison in (None, "nan", "negzero", "negative"):
                 aa, bb = a.copy(), b.copy()
-                if poison == "nan":
+                if poison == "negative":  # sign bits set: FMNMX3 loop instead of VIMNMX3
+                    aa = aa - np.float32(50)
+                elif poison == "nan":
                     aa[rng.random(m * k) < 0.01] = np.nan
                 elif poison == "negzero":
                     aa[rng.random(m * k) < 0.05] = -0.0
@@ -318,3 +320,20 @@ def test_launch_counter_advances():
     before = _native.launch_count()
     moa.inner(MoaArray((3, 3), range(9)), MoaArray((3, 3), range(9)))
     assert _native.launch_count() > before
+
+
+def test_streamed_host_path_bitwise_equals_one_launch(rng):
+    """Host operands of large products go through row blocks with overlapped
+    copies (kernel._execute_streamed); the bits equal one device launch."""
+    from paper_0907_0792_b200.kernel import _execute_streamed
+    m, k, n = 1000, 300, 777
+    a = rng.random(m * k) * 2 - 1
+    b = rng.random(k * n) * 2 - 1
+    for ops, dt in ((op_pair("multiply", "add"), np.float64), (op_pair("add", "min"), np.float32),
+                    (op_pair("max", "multiply"), np.float64)):
+        A, B = MoaArray((m, k), a, dtype=dt), MoaArray((k, n), b, dtype=dt)
+        want = moa.inner(A.to_device(), B.to_device(), ops).host_data()
+        for chunks in (2, 3, 7):
+            got = _execute_streamed(moa.plan_inner(A.shape, B.shape), A, B, ops, chunks)
+            assert got.shape == (m, n)
+            assert_bits_equal(got.data, want, f"{ops} chunks={chunks}")

@@ -58,6 +58,39 @@ __global__ void mix(float* out, float seed) {
   if (s == 12345.f) out[0] = s;
 }
 
+// register-tile microkernel: TI x TJ accumulators fed by TI a-pairs and TJ
+// b-pairs (the semiring kernel's inner loop without shared memory)
+template <int TI, int TJ, int ITERS>
+__global__ void tile(float* out, float seed) {
+  u64 ap[TI], bp[TJ];
+  float acc[TI][TJ];
+#pragma unroll
+  for (int i = 0; i < TI; i++) ap[i] = pack(seed + i + threadIdx.x, seed * i);
+#pragma unroll
+  for (int j = 0; j < TJ; j++) bp[j] = pack(j * 0.5f, j * 0.25f + seed);
+#pragma unroll
+  for (int i = 0; i < TI; i++)
+#pragma unroll
+    for (int j = 0; j < TJ; j++) acc[i][j] = 1e30f;
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < TI; i++)
+#pragma unroll
+      for (int j = 0; j < TJ; j++) {
+        u64 s = fadd2(ap[i], bp[j]);
+        acc[i][j] = __uint_as_float(__vimin3_u32(__float_as_uint(acc[i][j]), (unsigned)s, (unsigned)(s >> 32)));
+      }
+#pragma unroll
+    for (int i = 0; i < TI; i++) ap[i] += 0x0000000100000001ull;
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < TI; i++)
+#pragma unroll
+    for (int j = 0; j < TJ; j++) s += acc[i][j];
+  if (s == 12345.f) out[0] = s;
+}
+
 template <typename F>
 float timeit(F f, int reps) {
   cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
@@ -97,6 +130,21 @@ int main() {
   run<9>("fadd2_vimnmx3_units", 1, d, sms);
   run<10>("fadd2_half_fmnmx3_half_vimnmx3_units", 1, d, sms);
   run<11>("fadd2_3q_fmnmx3_1q_vimnmx3_units", 1, d, sms);
+  {
+    constexpr int IT = 1024;
+    auto tile_run = [&](const char* name, auto kern, int ti, int tj, int blocks, int threads) {
+      float ms = timeit([&] { kern<<<blocks, threads>>>(d, 1.0f); }, 5);
+      const double pairs = 2.0 * blocks * threads * (double)IT * ti * tj;
+      printf(", \"%s_Tpairs\": %.2f", name, pairs / (ms * 1e-3) / 1e12);
+    };
+    tile_run("tile8x8_16w", tile<8, 8, IT>, 8, 8, sms * 2, 256);
+    tile_run("tile8x8_8w", tile<8, 8, IT>, 8, 8, sms * 1, 256);
+    tile_run("tile4x8_32w", tile<4, 8, IT>, 4, 8, sms * 4, 256);
+    tile_run("tile4x8_16w", tile<4, 8, IT>, 4, 8, sms * 2, 256);
+    tile_run("tile4x4_64w", tile<4, 4, IT>, 4, 4, sms * 8, 256);
+    tile_run("tile4x4_32w", tile<4, 4, IT>, 4, 4, sms * 4, 256);
+    tile_run("tile8x4_32w", tile<8, 4, IT>, 8, 4, sms * 4, 256);
+  }
   printf("}\n");
   return 0;
 }

@@ -1,0 +1,74 @@
+// Instruction-order sweep for the float32 tropical fast loop at BASELINE
+// config 5's shape (tools; not part of the library).  Times each LOOP variant
+// of semiring_kernel and checks that all give identical bits.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//        -o tools/tune_semiring tools/tune_semiring.cu
+#include "../paper_0907_0792_b200/csrc/semiring.cu"
+
+#include <cstdio>
+
+std::atomic<uint64_t> moa::g_launches{0};
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+  fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1);} } while (0)
+
+__global__ void fill_tropical(float* p, size_t n, unsigned long long seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
+    const float u = (float)(x >> 40) * 0x1.0p-24f;
+    p[i] = ((x & 0xff) < 13) ? __int_as_float(0x7f800000) : u * 100.0f;  // ~5% +inf
+  }
+}
+__global__ void count_diff(const float* a, const float* b, size_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    c += (__float_as_int(a[i]) != __float_as_int(b[i]));
+  atomicAdd(out, c);
+}
+
+template <int LOOP>
+void trial(const moa::Problem& p0, float* out, float* ref, unsigned* special, unsigned long long* cnt) {
+  moa::Problem p = p0;
+  p.c = out;
+  cudaEvent_t s, e;
+  CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
+  CK((moa::semiring_launch<float, 0, 2, false, true, LOOP>(p, special)));
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 2; r++) {
+    CK(cudaEventRecord(s));
+    CK((moa::semiring_launch<float, 0, 2, false, true, LOOP>(p, special)));
+    CK(cudaEventRecord(e)); CK(cudaEventSynchronize(e));
+    float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
+  }
+  unsigned long long diff = 0;
+  if (out != ref) {
+    CK(cudaMemset(cnt, 0, 8));
+    count_diff<<<1184, 256>>>(out, ref, (size_t)p.M * p.N, cnt);
+    CK(cudaMemcpy(&diff, cnt, 8, cudaMemcpyDeviceToHost));
+  }
+  const double pairs = (double)p.M * p.N * p.K;
+  printf("{\"loop\": %d, \"ms\": %.3f, \"Gpairs_s\": %.1f, \"frac_of_24475\": %.4f, \"bit_diffs\": %llu}\n",
+         LOOP, best, pairs / (best * 1e-3) / 1e9, pairs / (best * 1e-3) / 1e9 / 24475.4, diff);
+  fflush(stdout);
+}
+
+int main() {
+  const int64_t n = 16384;
+  float *a, *b, *c, *ref;
+  unsigned* special;
+  unsigned long long* cnt;
+  CK(cudaMalloc(&a, n * n * 4)); CK(cudaMalloc(&b, n * n * 4));
+  CK(cudaMalloc(&c, n * n * 4)); CK(cudaMalloc(&ref, n * n * 4));
+  CK(cudaMalloc(&special, 8)); CK(cudaMalloc(&cnt, 8));
+  fill_tropical<<<1184, 256>>>(a, n * n, 11); fill_tropical<<<1184, 256>>>(b, n * n, 12);
+  unsigned flags[2] = {moa::S_PINF | moa::S_PZERO, moa::S_PINF | moa::S_PZERO};  // mode 2 data
+  CK(cudaMemcpy(special, flags, 8, cudaMemcpyHostToDevice));
+  moa::Problem p{MOA_DTYPE_F32, ref, a, b, n, n, n, n, n, n, 0, 2, false, 0};
+  trial<0>(p, ref, ref, special, cnt);
+  trial<1>(p, c, ref, special, cnt);
+  trial<2>(p, c, ref, special, cnt);
+  trial<3>(p, c, ref, special, cnt);
+  return 0;
+}
