@@ -189,6 +189,17 @@ def plan_for(w):
     return (plan_inner if w.mode == "inner" else plan_outer)(w.shape_a, w.shape_b)
 
 
+def job_plan(w, world: int):
+    """The whole job's plan: strong scaling splits one unit's rows over the
+    ranks; weak scaling stacks one unit per rank (world * M result rows, each
+    rank's block being exactly one unit, distributed.row_block)."""
+    from paper_0907_0792_b200.distributed import block_plan
+    plan = plan_for(w)
+    if SCALING[w.key] == "strong" or world == 1:
+        return plan
+    return block_plan(plan, 0, plan.noproc * world)
+
+
 def unit_amount(w, rows: int) -> float:
     """Algorithmic work of ``rows`` result rows in the metric's unit numerator."""
     m, k, n = w.mkn
@@ -248,11 +259,25 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
             step()
             e.record(stream)
         torch.cuda.synchronize(device)
-    launches = _native.launch_count() - launches0
+        launches = _native.launch_count() - launches0
+        step_ms = sum(s.elapsed_time(e) for s, e in evs)
+        # Short timed regions end before nvidia-smi samples them: keep the same
+        # load running (untimed, same count on every rank) until the sampler
+        # has seen ~0.4 s of it.
+        per = step_ms / steps
+        if world > 1:
+            t = torch.tensor([per], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            per = t.item()
+        extra = max(0, int(400.0 / max(per, 1e-3)) - steps)
+        for i in range(extra):
+            if i % 8 == 0:
+                flush()
+            step()
+        torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(device)
-    step_ms = sum(s.elapsed_time(e) for s, e in evs)
 
     # kernel-only: the dominant kernel's launch duration on its own stream
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -314,10 +339,12 @@ def measure_e2e(w, rows_range, a_pin, b_pin, steps, warmup, device, world, rank,
         def step():
             return fn(A, B, w.ops)
     else:
-        a_blk = a_pin[r0 * plan.lstride:r1 * plan.lstride]
+        gplan = job_plan(w, world)
+        a_blk = a_pin[r0 * plan.lstride:r1 * plan.lstride] if SCALING[w.key] == "strong" \
+            else a_pin  # weak scaling: this rank's unit is its whole A
 
         def step():
-            return sharded_product_host(plan, a_blk, b_pin if rank == 0 else None, w.ops,
+            return sharded_product_host(gplan, a_blk, b_pin if rank == 0 else None, w.ops,
                                         device=device, group=group)
     # results are returned in pinned host memory from torch's caching host
     # allocator; drop each step's result before the next so the cache reuses it

@@ -1,0 +1,135 @@
+"""The experiment harness and CLI (reference tests/test_bench.py, test_cli.py
+restated).  CPU tests exercise config validation, metrics, CSV formats and
+exit codes; GPU tests run real sweeps and one-off products."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_0907_0792_b200 import MoaArray, dump, harness, loads
+from paper_0907_0792_b200.cli import main
+from paper_0907_0792_b200.harness import (ExperimentConfig, ExperimentResult, MetricRow,
+                                          SizeFailure, TimingRecord, derive_metrics, emit_csv,
+                                          operand_pair, read_records_csv)
+
+
+def _rec(mode="moa-inner", threads=1, n=2, rep=0, secs=1.0, cs=3.5):
+    return TimingRecord(mode, threads, 8, n, rep, secs, cs)
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        ExperimentConfig(mode="nope")
+    with pytest.raises(ValueError):
+        ExperimentConfig(mode="moa-inner", workers=0)
+    with pytest.raises(ValueError):
+        ExperimentConfig(mode="moa-inner", ell=0)
+    with pytest.raises(ValueError):
+        ExperimentConfig(mode="moa-inner", repeats=0)
+    with pytest.raises(ValueError):
+        ExperimentConfig(mode="gemm-baseline", combine="add", reduce="min")
+    ExperimentConfig(mode="moa-outer", combine="add", reduce="min")
+
+
+def test_operand_pair_deterministic_and_shaped():
+    a1, b1 = operand_pair(3, 2, 8, 16)
+    a2, b2 = operand_pair(3, 2, 8, 16)
+    assert a1.shape == (2, 8) and b1.shape == (8, 16)
+    assert a1 == a2 and b1 == b2
+    assert np.all((a1.data >= 0) & (a1.data < 1))
+    # same generator as the reference's bench.operand_pair (bench.py:101-111)
+    gen = np.random.default_rng([3, 2, 8, 16])
+    np.testing.assert_array_equal(a1.data, gen.random((2, 8)).ravel())
+
+
+def test_derive_metrics_ratio_and_flag():
+    base = [_rec(threads=1, n=2, secs=1.0), _rec(threads=1, n=2, rep=1, secs=3.0)]
+    recs = [_rec(threads=2, n=2, secs=5.0), _rec(threads=2, n=2, rep=1, secs=5.0)]
+    rows = derive_metrics(recs, base)
+    assert rows == [MetricRow("moa-inner", 2, 2, 5.0, 4, 2.5, True)]
+    assert derive_metrics(base, base)[0].ratio == 1.0
+    with pytest.warns(UserWarning):
+        rows = derive_metrics([_rec(n=4)], [])
+    assert rows[0].ratio is None and rows[0].no_net_benefit is None
+
+
+def test_csv_round_trip_and_headers(tmp_path):
+    recs = [_rec(n=4, rep=1, secs=0.1, cs=1 / 3), _rec(n=2, secs=2e-5, cs=math.pi)]
+    p = tmp_path / "raw.csv"
+    emit_csv(p, recs)
+    lines = p.read_text().splitlines()
+    assert lines[0] == "mode,threads,ell,n,repeat,seconds,checksum"
+    back = read_records_csv(p)
+    assert back == sorted(recs, key=lambda r: (r.mode, r.threads, r.n, r.repeat))
+    m = tmp_path / "m.csv"
+    emit_csv(m, derive_metrics(recs, recs))
+    assert m.read_text().splitlines()[0] == \
+        "mode,threads,n,mean_seconds,total_x,ratio,no_net_benefit"
+    emit_csv(tmp_path / "empty.csv", [], kind="metrics")
+    assert (tmp_path / "empty.csv").read_text().startswith("mode,threads,n,mean_seconds")
+    with pytest.raises(ValueError):
+        emit_csv(tmp_path / "x.csv", recs, kind="bogus")
+
+
+def test_cli_bad_bounds_and_failure_exit_codes(tmp_path, monkeypatch, capsys):
+    out = tmp_path / "raw.csv"
+    assert main(["bench", "--mode", "moa-inner", "--n-min", "5", "--n-max", "2",
+                 "--out", str(out)]) == 2
+    assert "bad sweep bounds" in capsys.readouterr().err
+    result = ExperimentResult(records=[], failures=[SizeFailure("moa-inner", 1, 8, 4, "OOM")])
+    monkeypatch.setattr(harness, "run_experiment", lambda cfg: result)
+    args = ["bench", "--mode", "moa-inner", "--out", str(out)]
+    assert main(args) == 1
+    assert main(args + ["--keep-going"]) == 0
+
+
+def test_cli_metrics_command(tmp_path):
+    raw1, raw2, out = tmp_path / "r1.csv", tmp_path / "r2.csv", tmp_path / "m.csv"
+    emit_csv(raw1, [_rec(threads=1, n=n, secs=1.0) for n in (2, 4)])
+    emit_csv(raw2, [_rec(threads=2, n=n, secs=1.5) for n in (2, 4)])
+    assert main(["metrics", "--raw", str(raw2), "--baseline-raw", str(raw1),
+                 "--out", str(out)]) == 0
+    cells = [ln.split(",") for ln in out.read_text().splitlines()[1:]]
+    assert [c[5] for c in cells] == ["1.5", "1.5"]
+    assert [c[6] for c in cells] == ["false", "false"]
+
+
+# ---- on the GPU ----------------------------------------------------------------
+
+@pytest.mark.gpu
+def test_sweep_modes_and_checksums(tmp_path):
+    raws = {}
+    for mode in ("moa-inner", "gemm-baseline"):
+        out = tmp_path / f"{mode}.csv"
+        assert main(["bench", "--mode", mode, "--threads", "2", "--ell", "128", "--n-min", "1",
+                     "--n-max", "8", "--repeats", "2", "--seed", "9", "--out", str(out)]) == 0
+        raws[mode] = read_records_csv(out)
+        assert [r.n for r in raws[mode]] == [2**p for p in range(1, 9) for _ in range(2)]
+        assert all(r.seconds > 0 and r.threads == 2 for r in raws[mode])
+    for x, y in zip(raws["moa-inner"], raws["gemm-baseline"]):
+        assert x.n == y.n and x.checksum == pytest.approx(y.checksum, rel=1e-12)
+    outer = tmp_path / "outer.csv"
+    assert main(["bench", "--mode", "moa-outer", "--ell", "1", "--n-max", "4",
+                 "--combine", "add", "--reduce", "min", "--repeats", "1",
+                 "--out", str(outer)]) == 0
+    assert len(read_records_csv(outer)) == 4
+
+
+@pytest.mark.gpu
+def test_product_command_matches_api(tmp_path, capsys):
+    import paper_0907_0792_b200 as moa
+    left, right = tmp_path / "a.txt", tmp_path / "b.txt"
+    dump(MoaArray((2, 3), [1, 2, 3, 4, 5, 6]), left)
+    dump(MoaArray((3, 4), range(12)), right)
+    assert main(["product", "--mode", "inner", "--left", str(left), "--right", str(right)]) == 0
+    got = loads(capsys.readouterr().out)
+    assert got.shape == (2, 4) and got.data.tolist() == [32, 38, 44, 50, 68, 83, 98, 113]
+    dump(MoaArray((2,), [1, 2]), left)
+    dump(MoaArray((2,), [10, 20]), right)
+    out = tmp_path / "c.txt"
+    assert main(["product", "--mode", "inner", "--left", str(left), "--right", str(right),
+                 "--combine", "add", "--reduce", "min", "--threads", "3", "--out", str(out)]) == 0
+    assert moa.load(out).item() == 11.0

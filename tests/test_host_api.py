@@ -273,3 +273,23 @@ def test_distributed_row_block_matches_row_blocks():
         for world in (1, 2, 4, 8):
             got = [range(*row_block(noproc, world, r)) for r in range(world)]
             assert got == moa.row_blocks(noproc, world)
+
+
+def test_bench_job_plans_match_rank_blocks():
+    """bench.py's multi-rank plans: weak scaling gives every rank exactly one
+    unit of rows, strong scaling splits one unit (checked without a GPU)."""
+    import bench
+    from paper_0907_0792_b200.distributed import row_block
+    from paper_0907_0792_b200.workloads import WORKLOADS
+    for key in ("c2", "c4"):
+        w = WORKLOADS[key]
+        m = w.mkn[0]
+        for world in (1, 2, 4, 8):
+            plan = bench.job_plan(w, world)
+            blocks = [row_block(plan.noproc, world, r) for r in range(world)]
+            if bench.SCALING[key] == "weak":
+                assert plan.noproc == m * world
+                assert all(r1 - r0 == m for r0, r1 in blocks)
+            else:
+                assert plan.noproc == m
+                assert sum(r1 - r0 for r0, r1 in blocks) == m

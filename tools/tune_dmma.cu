@@ -88,6 +88,12 @@ int main() {
     trial<DmmaCfg<32, 32, 16, 16, 3, 32>>("32x32_w16x16_s3_bk32", sh, A, B, C, Cref, d_cnt, false);
     trial<DmmaCfg<32, 32, 16, 16, 6>>("32x32_w16x16_s6_bk16", sh, A, B, C, Cref, d_cnt, false);
     trial<DmmaCfg<16, 32, 16, 16, 4>>("16x32_w16x16_s4_bk16", sh, A, B, C, Cref, d_cnt, false);
+    if (sh.K <= 512) {
+      trial<DmmaCfg<32, 32, 16, 16, 8, 32>>("32x32_w16x16_s8_bk32", sh, A, B, C, Cref, d_cnt, false);
+      trial<DmmaCfg<16, 32, 16, 16, 8, 32>>("16x32_w16x16_s8_bk32", sh, A, B, C, Cref, d_cnt, false);
+      trial<DmmaCfg<32, 32, 16, 16, 5, 64>>("32x32_w16x16_s5_bk64", sh, A, B, C, Cref, d_cnt, false);
+      trial<DmmaCfg<32, 16, 16, 16, 8, 32>>("32x16_w16x16_s8_bk32", sh, A, B, C, Cref, d_cnt, false);
+    }
     CK(cudaFree(A)); CK(cudaFree(B)); CK(cudaFree(C)); CK(cudaFree(Cref)); CK(cudaFree(d_cnt));
   }
   return 0;
