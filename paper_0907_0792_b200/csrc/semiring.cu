@@ -110,7 +110,11 @@ __device__ __forceinline__ float fold3(float acc, float s0, float s1) {
 // LOOP selects the instruction order of the fast loop's 8x8 tile (tuning):
 // 0: element by element; 1: per row, 8 FADD2 then 8 folds; 2: column-major;
 // 3: per row, two batches of 4 FADD2 + 4 folds.  All orders give the same bits.
-template <typename T, int C, int R, bool ACC, bool FASTCAND, int LOOP = MOA_SEMIRING_LOOP>
+// MODEK: -1 = exact fold only (no pre-scan); for the tropical candidates the
+// host launches one specialisation per fold mode (2 = VIMNMX3, 1 = FMNMX3,
+// 0 = exact) and each returns at once unless the device-side pre-scan selected
+// it — one loop per kernel keeps register pressure (and spills) down.
+template <typename T, int C, int R, bool ACC, int MODEK, int LOOP = MOA_SEMIRING_LOOP>
 __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
     semiring_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ b,
                     int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
@@ -133,8 +137,9 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
   const int tid = threadIdx.x;
   const int ty = tid >> 4, tx = tid & 15;
 
-  int mode = 0;  // 0 exact, 1 FMNMX3, 2 VIMNMX3 (see tropical_fold_mode)
-  if (FASTCAND && !ACC) mode = tropical_fold_mode(C, __ldg(special), __ldg(special + 1));
+  if constexpr (MODEK >= 0) {
+    if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODEK) return;
+  }
 
   // ---- accumulators: rows ty*8+i, columns 32*(j>>1) + 2*tx + (j&1) ----
   A acc[8][8];
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
   // The unsigned-order fold (mode 2) cannot start from -inf (sign bit set).
   // Mode 2 implies every combine result is >= +0 and K >= 2, so a max fold
   // from +0 gives the same bits as one from the identity.
-  if (FASTCAND && R == R_MAX && mode == 2) {
+  if constexpr (R == R_MAX && MODEK == 2) {
 #pragma unroll
     for (int i = 0; i < 8; i++)
 #pragma unroll
@@ -213,8 +218,8 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
     const int64_t krem = K - kt * BK;
     const int kend = krem < BK ? (int)krem : BK;
 
-    if (FASTCAND && mode != 0) {
-      if constexpr (FASTCAND && sizeof(T) == 4) {
+    if constexpr (MODEK >= 1) {
+      if constexpr (sizeof(T) == 4) {
         auto fast_tile = [&](auto intfold) {
           constexpr bool INTFOLD = decltype(intfold)::value;
           auto fast_pair = [&](int kp) {
@@ -285,8 +290,7 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
             }
           }
         };
-        if (C == C_ADD && mode == 2) fast_tile(std::true_type{});
-        else fast_tile(std::false_type{});
+        fast_tile(std::integral_constant<bool, MODEK == 2>{});
       }
     } else {
       // exact loop: the reference's fold, k ascending, k beyond K skipped
@@ -356,9 +360,9 @@ void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* o
   count_launch();
 }
 
-template <typename T, int C, int R, bool ACC, bool FASTCAND, int LOOP = MOA_SEMIRING_LOOP>
+template <typename T, int C, int R, bool ACC, int MODEK, int LOOP = MOA_SEMIRING_LOOP>
 cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
-  auto kern = semiring_kernel<T, C, R, ACC, FASTCAND, LOOP>;
+  auto kern = semiring_kernel<T, C, R, ACC, MODEK, LOOP>;
   const size_t smem = SemiringShape<T, R>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -374,7 +378,7 @@ cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
 
 template <typename T, int C, int R>
 cudaError_t semiring_acc(const Problem& p) {
-  if (p.accumulate) return semiring_launch<T, C, R, true, false>(p, nullptr);
+  if (p.accumulate) return semiring_launch<T, C, R, true, -1>(p, nullptr);
   constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB) &&
                         (R == R_MIN || R == R_MAX);
   if constexpr (cand) {
@@ -386,11 +390,14 @@ cudaError_t semiring_acc(const Problem& p) {
     if (e != cudaSuccess) return e;
     launch_scan<T>(static_cast<const T*>(p.a), p.M, p.K, p.lda, special, p.stream);
     launch_scan<T>(static_cast<const T*>(p.b), p.K, p.N, p.ldb, special + 1, p.stream);
-    e = semiring_launch<T, C, R, false, true>(p, special);
+    // one specialisation per fold mode; all but the selected one exit at once
+    if constexpr (C == C_ADD) e = semiring_launch<T, C, R, false, 2>(p, special);
+    if (e == cudaSuccess) e = semiring_launch<T, C, R, false, 1>(p, special);
+    if (e == cudaSuccess) e = semiring_launch<T, C, R, false, 0>(p, special);
     cudaError_t e2 = cudaFreeAsync(special, p.stream);
     return e != cudaSuccess ? e : e2;
   } else {
-    return semiring_launch<T, C, R, false, false>(p, nullptr);
+    return semiring_launch<T, C, R, false, -1>(p, nullptr);
   }
 }
 
