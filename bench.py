@@ -452,6 +452,9 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-inner", action="store_true", help="skip the extra inner-product legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N>1 (gloo only to exercise the "
+                         "multi-rank code path on fewer GPUs than ranks; timings meaningless)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -461,9 +464,13 @@ def main() -> None:
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     w = WORKLOADS[args.config]
