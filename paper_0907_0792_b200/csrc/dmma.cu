@@ -29,8 +29,6 @@ namespace moa {
 
 namespace {
 
-constexpr int DGROUP_M = 8;
-
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -58,10 +56,13 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int BK_ = 16, int MINB_ = 1>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int BK_ = 16, int MINB_ = 1,
+          bool PF_ = false, int GM_ = 8>
 struct DmmaCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
   static constexpr int DBK = BK_, MIN_BLOCKS = MINB_;
+  static constexpr bool PREFETCH = PF_;  // load the next k4 step's fragments before the MMAs
+  static constexpr int GROUP_M = GM_;    // row tiles per rasterisation group
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
   static constexpr int MI = WM / 16, NI = WN / 8;
@@ -85,9 +86,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
   double* Bs = dsm + STAGES * Cfg::A_STAGE;
 
   const int64_t pid = blockIdx.x;
-  const int64_t width = DGROUP_M * tiles_n;
-  const int64_t first_m = (pid / width) * DGROUP_M;
-  const int64_t gsize = (tiles_m - first_m) < DGROUP_M ? (tiles_m - first_m) : DGROUP_M;
+  constexpr int GM = Cfg::GROUP_M;
+  const int64_t width = GM * tiles_n;
+  const int64_t first_m = (pid / width) * GM;
+  const int64_t gsize = (tiles_m - first_m) < GM ? (tiles_m - first_m) : GM;
   const int64_t m0 = (first_m + (pid % width) % gsize) * BM;
   const int64_t n0 = ((pid % width) / gsize) * BN;
 
@@ -162,20 +164,50 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MIN_BLOCKS)
     }
     const double* as = As + (int)(kt % STAGES) * Cfg::A_STAGE + (wm0 + g) * LDA_S + t;
     const double* bs = Bs + (int)(kt % STAGES) * Cfg::B_STAGE + t * LDB_S + wn0 + g;
+    if constexpr (!Cfg::PREFETCH) {
 #pragma unroll
-    for (int kk = 0; kk < DBK; kk += 4) {
-      double af[MI][2], bf[NI];
+      for (int kk = 0; kk < DBK; kk += 4) {
+        double af[MI][2], bf[NI];
+#pragma unroll
+        for (int mi = 0; mi < MI; mi++) {
+          af[mi][0] = as[(mi * 16) * LDA_S + kk];
+          af[mi][1] = as[(mi * 16 + 8) * LDA_S + kk];
+        }
+#pragma unroll
+        for (int ni = 0; ni < NI; ni++) bf[ni] = bs[kk * LDB_S + ni * 8];
+#pragma unroll
+        for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+          for (int ni = 0; ni < NI; ni++) dmma_16x8x4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+      }
+    } else {
+      // software-pipelined fragments: step kk's MMAs issue while kk+4's loads fly
+      double af[2][MI][2], bf[2][NI];
 #pragma unroll
       for (int mi = 0; mi < MI; mi++) {
-        af[mi][0] = as[(mi * 16) * LDA_S + kk];
-        af[mi][1] = as[(mi * 16 + 8) * LDA_S + kk];
+        af[0][mi][0] = as[(mi * 16) * LDA_S];
+        af[0][mi][1] = as[(mi * 16 + 8) * LDA_S];
       }
 #pragma unroll
-      for (int ni = 0; ni < NI; ni++) bf[ni] = bs[kk * LDB_S + ni * 8];
+      for (int ni = 0; ni < NI; ni++) bf[0][ni] = bs[ni * 8];
 #pragma unroll
-      for (int mi = 0; mi < MI; mi++)
+      for (int kk = 0; kk < DBK; kk += 4) {
+        const int cur = (kk / 4) & 1, nxt = cur ^ 1;
+        if (kk + 4 < DBK) {
 #pragma unroll
-        for (int ni = 0; ni < NI; ni++) dmma_16x8x4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+          for (int mi = 0; mi < MI; mi++) {
+            af[nxt][mi][0] = as[(mi * 16) * LDA_S + kk + 4];
+            af[nxt][mi][1] = as[(mi * 16 + 8) * LDA_S + kk + 4];
+          }
+#pragma unroll
+          for (int ni = 0; ni < NI; ni++) bf[nxt][ni] = bs[(kk + 4) * LDB_S + ni * 8];
+        }
+#pragma unroll
+        for (int mi = 0; mi < MI; mi++)
+#pragma unroll
+          for (int ni = 0; ni < NI; ni++)
+            dmma_16x8x4(acc[mi][ni], af[cur][mi][0], af[cur][mi][1], bf[cur][ni]);
+      }
     }
   }
   cp_async_wait<0>();

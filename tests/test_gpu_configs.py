@@ -114,3 +114,39 @@ def test_c5_rows_sharded_any_gpu_count_bitwise():
             r0, r1 = rows.start, rows.stop
             sub = moa.inner(MoaArray((r1 - r0, k), A.data[r0 * k:r1 * k]), B, w.ops)
             assert torch.equal(sub.data, full[r0 * n:r1 * n])
+
+
+def test_index_math_beyond_2_31_elements():
+    """Results with more than 2^31 elements (64-bit offsets in every kernel):
+    the last rows, where 32-bit offsets would wrap, match the oracle."""
+    import torch
+    from paper_0907_0792_b200.kernel import launch, plan_inner, plan_outer
+    rng = np.random.default_rng(5)
+    # outer product, float32: 70000 x 32768 = 2.29e9 elements
+    m, n = 70000, 32768
+    a = rng.random(m, dtype=np.float32)
+    b = rng.random(n, dtype=np.float32)
+    c = torch.empty(m * n, dtype=torch.float32, device="cuda")
+    launch(plan_outer((m,), (n,)), c, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+           moa.op_pair("add", "max"))
+    tail = c[(m - 3) * n:].cpu().numpy().reshape(3, n)
+    assert_bits_equal(tail, (a[-3:, None] + b[None, :]).astype(np.float32))
+    del c
+    # inner products with M*N > 2^31: DMMA (f64) and tropical (f32)
+    for ops, dt, (m, k, n) in ((moa.MUL_ADD, np.float64, (50000, 8, 45000)),
+                               (moa.op_pair("add", "min"), np.float32, (50000, 6, 45000))):
+        a = rng.random(m * k).astype(dt)
+        b = rng.random(k * n).astype(dt)
+        tdt = torch.float64 if dt == np.float64 else torch.float32
+        c = torch.empty(m * n, dtype=tdt, device="cuda")
+        launch(plan_inner((m, k), (k, n)), c, torch.from_numpy(a).cuda(),
+               torch.from_numpy(b).cuda(), ops)
+        got = c[(m - 2) * n:].cpu().numpy()
+        comb, red = ops.codes()
+        want = oracle.product(a[(m - 2) * k:], b, 2, k, n, comb, red)
+        if dt == np.float64:
+            assert_within(got, want, sum_tolerance(k, a, b))
+        else:
+            assert_bits_equal(got, want.astype(np.float32))
+        del c
+        torch.cuda.empty_cache()

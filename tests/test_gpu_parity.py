@@ -337,3 +337,32 @@ def test_streamed_host_path_bitwise_equals_one_launch(rng):
             got = _execute_streamed(moa.plan_inner(A.shape, B.shape), A, B, ops, chunks)
             assert got.shape == (m, n)
             assert_bits_equal(got.data, want, f"{ops} chunks={chunks}")
+
+
+def test_kernels_never_write_outside_their_rows(rng):
+    """Canary check (compute-sanitizer is closed on this pool): every route
+    writes exactly the result elements of its rows — sentinels before, after
+    and between the owned rows stay untouched."""
+    torch = _torch()
+    sentinel = -12345.678
+    cases = [((70, 33, 45), op_pair("multiply", "add")), ((70, 33, 45), op_pair("add", "min")),
+             ((70, 1, 257), op_pair("multiply", "add")), ((70, 0, 45), op_pair("add", "max")),
+             ((129, 20, 131), op_pair("divide", "multiply")), ((5, 40, 2048), op_pair("min", "max"))]
+    for (m, k, n), ops in cases:
+        for dt in (torch.float64, torch.float32):
+            a = _dev(rng.random(m * k) * 2 - 1, dt)
+            b = _dev(rng.random(k * n) * 2 - 1, dt)
+            plan = plan_inner((m, k), (k, n))
+            pad = 37
+            buf = torch.full((m * n + 2 * pad,), sentinel, dtype=dt, device="cuda")
+            launch(plan, buf[pad:pad + m * n], a, b, ops, start=1, step=3)
+            host = buf.cpu().numpy()
+            want_sent = np.ones(m * n + 2 * pad, dtype=bool)
+            for i in range(1, m, 3):
+                want_sent[pad + i * n:pad + (i + 1) * n] = False
+            got_sent = host == np.array(sentinel, dtype=host.dtype)
+            assert np.array_equal(got_sent[want_sent], np.ones(want_sent.sum(), bool)), \
+                f"write outside owned rows {(m, k, n)} {ops} {dt}"
+            owned = host[~want_sent]
+            assert not np.any(owned == np.array(sentinel, dtype=host.dtype)), \
+                f"owned element left unwritten {(m, k, n)} {ops} {dt}"

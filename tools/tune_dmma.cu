@@ -76,23 +76,18 @@ int main() {
     CK(cudaMalloc(&d_cnt, 8));
     fill_uniform<<<1184, 256>>>(A, sh.M * sh.K, 1); fill_uniform<<<1184, 256>>>(B, sh.K * sh.N, 2);
     using namespace moa;
-    trial<DmmaCfg<128, 128, 64, 32, 4>>("128x128_w64x32_s4_bk16", sh, A, B, C, Cref, d_cnt, true);
-    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2>>("64x128_w32x32_s4_bk16_2cta", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 128, 32, 32, 3, 16, 2>>("64x128_w32x32_s3_bk16_2cta", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 64, 32, 32, 3, 16, 3>>("64x64_w32x32_s3_bk16_3cta", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 64, 32, 32, 4, 16, 3>>("64x64_w32x32_s4_bk16_3cta", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 64, 32, 32, 2, 32, 3>>("64x64_w32x32_s2_bk32_3cta", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<32, 128, 32, 32, 3, 16, 3>>("32x128_w32x32_s3_bk16_3cta", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 128, 32, 32, 2, 32, 2>>("64x128_w32x32_s2_bk32_2cta", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<32, 32, 16, 16, 4>>("32x32_w16x16_s4_bk16", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2>>("64x128_w32x32_s4_bk16_2cta", sh, A, B, C, Cref, d_cnt, true);
+    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, true>>("64x128_..._prefetch", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>>("64x128_..._group16", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 4>>("64x128_..._group4", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, true, 16>>("64x128_..._prefetch_group16", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<64, 128, 32, 32, 3, 32, 2, true>>("64x128_s3_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<64, 64, 32, 32, 3, 16, 3, true>>("64x64_s3_3cta_prefetch", sh, A, B, C, Cref, d_cnt, false);
     trial<DmmaCfg<32, 32, 16, 16, 3, 32>>("32x32_w16x16_s3_bk32", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<32, 32, 16, 16, 6>>("32x32_w16x16_s6_bk16", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<16, 32, 16, 16, 4>>("16x32_w16x16_s4_bk16", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<32, 32, 16, 16, 3, 32, 1, true>>("32x32_w16x16_s3_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
     if (sh.K <= 512) {
-      trial<DmmaCfg<32, 32, 16, 16, 8, 32>>("32x32_w16x16_s8_bk32", sh, A, B, C, Cref, d_cnt, false);
-      trial<DmmaCfg<16, 32, 16, 16, 8, 32>>("16x32_w16x16_s8_bk32", sh, A, B, C, Cref, d_cnt, false);
-      trial<DmmaCfg<32, 32, 16, 16, 5, 64>>("32x32_w16x16_s5_bk64", sh, A, B, C, Cref, d_cnt, false);
-      trial<DmmaCfg<32, 16, 16, 16, 8, 32>>("32x16_w16x16_s8_bk32", sh, A, B, C, Cref, d_cnt, false);
+      trial<DmmaCfg<16, 16, 16, 16, 8, 32, 1, true>>("16x16_w16x16_s8_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
+      trial<DmmaCfg<16, 32, 16, 16, 8, 32, 1, true>>("16x32_w16x16_s8_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
     }
     CK(cudaFree(A)); CK(cudaFree(B)); CK(cudaFree(C)); CK(cudaFree(Cref)); CK(cudaFree(d_cnt));
   }
