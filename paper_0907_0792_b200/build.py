@@ -23,7 +23,8 @@ LIB_PATH = PKG_DIR / LIB_NAME
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
-              "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
+              "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr",
+              "-diag-suppress", "177"]
 
 
 def _nvcc() -> str:

@@ -5,27 +5,29 @@
 //     for i in rows: for l < rowsinred: av = a[l + i*lstride]
 //         for j < elsinop: res[i*restride+j] = reduce(res[..], combine(av, b[l*rstride+j]))
 // Every result element is an l-ascending fold from the identity.  Rows (and
-// elements) are independent, so the GPU tiles C into 128x128 blocks and gives
-// each thread an 8x8 register tile; each thread still folds its elements over
-// l in ascending order with the reference's exact operations, which makes the
-// result bit-identical to the reference for every pair (the "exact" loop).
+// elements) are independent, so the GPU tiles C into (16*TM) x (16*TN) blocks
+// of 16x16 threads with a TM x TN register tile each; each thread folds its
+// elements over l in ascending order with the reference's exact operations,
+// which makes the result bit-identical to the reference for every pair (the
+// "exact" loop).
 //
 // For combine in {add, subtract} with reduce in {min, max} on float32 — the
 // tropical semirings, BASELINE config 5 — the exact loop costs a FADD, FSETP
-// and FSEL per pair.  The fast loop instead adds two contraction steps at once
-// with a packed FADD2 and folds both sums with one 3-input FMNMX3 (about 2.5x
-// the pair rate, tools/peaks.cu).  FMNMX3 prefers non-NaN operands and may
-// order +-0 freely, so it is bit-exact only when no combine result is NaN or
-// -0.0.  A pre-scan kernel records which special values occur in A and B and
-// the main kernel picks the loop on the device (fast_fold_is_exact), so no
-// host synchronisation is needed and the result never depends on the choice.
+// and FSEL per pair.  The fast loops add two contraction steps at once with a
+// packed FADD2 and fold both sums with one 3-input min/max: VIMNMX3 on the bit
+// patterns when every combine result is a non-negative float, FMNMX3 when no
+// combine result can be NaN or -0.0 (moa_common.cuh).  A pre-scan kernel
+// records which special values occur in A and B; the host launches one kernel
+// specialisation per fold mode and all but the one the device flags select
+// return at once, so there is no host synchronisation and the result never
+// depends on the choice.
 //
 // Shared-memory layout: both tiles are stored as k-PAIRS, As[kp][m] =
 // (A[m][2kp], A[m][2kp+1]) and Bs[kp][n] = (B[2kp][n], B[2kp+1][n]), so a
 // thread's FADD2 operands are single 64-bit LDS results.  Thread (ty, tx) owns
-// rows ty*8..ty*8+7 and columns 32g + 2tx + {0,1} (g < 4): A reads are
+// rows ty*TM..ty*TM+TM-1 and columns 32g + 2tx + {0,1} (g < TN/2): A reads are
 // warp-broadcasts, B reads are 16-byte loads over a contiguous 256-byte span
-// (conflict-free).  Global->shared staging is register double-buffered.
+// (conflict-free).  Global->shared staging is element-wise cp.async (3 stages).
 #include <type_traits>
 
 #include "moa_common.cuh"
@@ -36,26 +38,33 @@ namespace moa {
 
 namespace {
 
-constexpr int SBM = 128, SBN = 128, SNT = 256, GROUP_M = 8;
+constexpr int SNT = 256, GROUP_M = 8;  // 16 x 16 threads per CTA
 
 template <typename T> struct alignas(2 * sizeof(T)) KPair { T x, y; };
 
-// float32 min/max tiles keep 64 float accumulators and run two CTAs per SM
-// (16 warps); float64 or float64-accumulated tiles need twice the registers.
-template <typename T, int R> struct SemiringShape {
+template <typename T, int R, int TM_, int TN_, int MINB_>
+struct SemiringShape {
   static constexpr bool F4 = sizeof(typename AccType<T, R>::type) == 4;
+  static constexpr int TM = TM_, TN = TN_;
+  static constexpr int BM = 16 * TM, BN = 16 * TN;
   static constexpr int BK = F4 ? 32 : 16;       // k per stage (one barrier per BK)
   static constexpr int KP = BK / 2;             // k-pairs per stage
   static constexpr int STAGES = 3;
-  static constexpr int MIN_BLOCKS = F4 ? 2 : 1;
-  static constexpr int A_STAGE = KP * SBM;      // pairs
-  static constexpr int B_STAGE = KP * SBN;      // pairs
+  static constexpr int A_STAGE = KP * BM;       // pairs
+  static constexpr int B_STAGE = KP * BN;       // pairs
   static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(KPair<T>);
   // element-wise loader: thread t copies A elements (row t/BK + (SNT/BK)*q, k t%BK)
-  // and B elements (k t/SBN + (SNT/SBN)*q, column t%SBN)
-  static constexpr int QA = SBM * BK / SNT, A_RSTEP = SNT / BK;
-  static constexpr int QB = BK * SBN / SNT, B_KSTEP = SNT / SBN;
-  static_assert(QA <= 32 && B_KSTEP == 2, "loader layout");
+  // and B elements (k t/BN + (SNT/BN)*q, column t%BN)
+  static constexpr int QA = BM * BK / SNT, A_RSTEP = SNT / BK;
+  static constexpr int QB = BK * BN / SNT, B_KSTEP = SNT / BN;
+  static_assert(QA <= 32 && B_KSTEP % 2 == 0 && TM % 2 == 0 && TN % 2 == 0, "tile layout");
+};
+
+// Default tiles: float32 min/max (c5): 8x8 per thread, two CTAs per SM
+// (tools/tune_semiring.cu); float64 or float64-accumulated: 8x8, one CTA.
+template <typename T, int R> struct DefaultTile {
+  static constexpr bool F4 = sizeof(typename AccType<T, R>::type) == 4;
+  static constexpr int TM = 8, TN = 8, MINB = F4 ? 2 : 1;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -103,25 +112,22 @@ __device__ __forceinline__ float fold3(float acc, float s0, float s1) {
   return r;
 }
 
-#ifndef MOA_SEMIRING_LOOP
-#define MOA_SEMIRING_LOOP 0
-#endif
-
-// LOOP selects the instruction order of the fast loop's 8x8 tile (tuning):
-// 0: element by element; 1: per row, 8 FADD2 then 8 folds; 2: column-major;
-// 3: per row, two batches of 4 FADD2 + 4 folds.  All orders give the same bits.
-// MODEK: -1 = exact fold only (no pre-scan); for the tropical candidates the
-// host launches one specialisation per fold mode (2 = VIMNMX3, 1 = FMNMX3,
-// 0 = exact) and each returns at once unless the device-side pre-scan selected
-// it — one loop per kernel keeps register pressure (and spills) down.
-template <typename T, int C, int R, bool ACC, int MODEK, int LOOP = MOA_SEMIRING_LOOP>
-__global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
+// MODEK: -1 = exact fold only (no pre-scan); 0 / 1 / 2 = the exact / FMNMX3 /
+// VIMNMX3 specialisation of a tropical candidate, which returns at once unless
+// the device-side pre-scan selected that mode (one loop per kernel keeps
+// register pressure down).
+template <typename T, int C, int R, bool ACC, int MODEK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__(SNT, MINB)
     semiring_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ b,
                     int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                     const unsigned* special, int64_t tiles_m, int64_t tiles_n) {
   using A = typename AccType<T, R>::type;
-  using Shape = SemiringShape<T, R>;
-  constexpr int STAGES = Shape::STAGES;
+  using Shape = SemiringShape<T, R, TM, TN, MINB>;
+  constexpr int STAGES = Shape::STAGES, BM = Shape::BM, BN = Shape::BN;
+  constexpr int BK = Shape::BK, KP = Shape::KP;
+  if constexpr (MODEK >= 0) {
+    if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODEK) return;
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KPair<T>* As = reinterpret_cast<KPair<T>*>(smem_raw);
   KPair<T>* Bs = As + STAGES * Shape::A_STAGE;
@@ -131,23 +137,19 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
   const int64_t width = GROUP_M * tiles_n;
   const int64_t first_m = (pid / width) * GROUP_M;
   const int64_t gsize = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
-  const int64_t m0 = (first_m + (pid % width) % gsize) * SBM;
-  const int64_t n0 = ((pid % width) / gsize) * SBN;
+  const int64_t m0 = (first_m + (pid % width) % gsize) * BM;
+  const int64_t n0 = ((pid % width) / gsize) * BN;
 
   const int tid = threadIdx.x;
   const int ty = tid >> 4, tx = tid & 15;
 
-  if constexpr (MODEK >= 0) {
-    if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODEK) return;
-  }
-
-  // ---- accumulators: rows ty*8+i, columns 32*(j>>1) + 2*tx + (j&1) ----
-  A acc[8][8];
+  // ---- accumulators: rows ty*TM+i, columns 32*(j>>1) + 2*tx + (j&1) ----
+  A acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 8; i++)
+  for (int i = 0; i < TM; i++)
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
-      const int64_t row = m0 + ty * 8 + i;
+    for (int j = 0; j < TN; j++) {
+      const int64_t row = m0 + ty * TM + i;
       const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
       if (ACC && row < M && col < N)
         acc[i][j] = A(c[row * ldc + col]);
@@ -159,16 +161,15 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
   // from +0 gives the same bits as one from the identity.
   if constexpr (R == R_MAX && MODEK == 2) {
 #pragma unroll
-    for (int i = 0; i < 8; i++)
+    for (int i = 0; i < TM; i++)
 #pragma unroll
-      for (int j = 0; j < 8; j++) acc[i][j] = A(0);
+      for (int j = 0; j < TN; j++) acc[i][j] = A(0);
   }
 
   // ---- element-wise async copies into the k-pair layouts (zero-filled outside) ----
   // Per-thread bases are fixed for the whole kernel; a stage only adds k0.
-  constexpr int BK = Shape::BK, KP = Shape::KP;
   const int a_kk = tid % BK, a_r = tid / BK;
-  const int b_n = tid % SBN, b_kk = tid / SBN;
+  const int b_n = tid % BN, b_kk = tid / BN;
   const T* a_src = a + (m0 + a_r) * lda + a_kk;
   const int64_t a_qstep = (int64_t)Shape::A_RSTEP * lda;
   const T* b_src = b + (int64_t)b_kk * ldb + n0 + b_n;
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
   for (int q = 0; q < Shape::QA; q++)
     if (m0 + a_r + q * Shape::A_RSTEP < M) a_rows_ok |= 1u << q;
   const bool b_col_ok = n0 + b_n < N;
-  const int a_dst = 2 * ((a_kk >> 1) * SBM + a_r) + (a_kk & 1);   // in T elements
-  const int b_dst = 2 * b_n + b_kk;                                // in T elements
+  const int a_dst = 2 * ((a_kk >> 1) * BM + a_r) + (a_kk & 1);             // T elements
+  const int b_dst = 2 * ((b_kk >> 1) * BN + b_n) + (b_kk & 1);             // T elements
   auto load_stage = [&](int stage, int64_t k0) {
     T* as = reinterpret_cast<T*>(As + stage * Shape::A_STAGE) + a_dst;
     T* bs = reinterpret_cast<T*>(Bs + stage * Shape::B_STAGE) + b_dst;
@@ -188,13 +189,15 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
 #pragma unroll
     for (int q = 0; q < Shape::QA; q++) {
       const bool ok = a_k_ok && ((a_rows_ok >> q) & 1u);
-      cp_async_elem<sizeof(T)>(as + 2 * Shape::A_RSTEP * q, ok ? pa + q * a_qstep : a, ok);
+      cp_async_elem<sizeof(T)>(as + 2 * Shape::A_RSTEP * q,
+                               ok ? pa + q * a_qstep : a, ok);
     }
     const T* pb = b_src + k0 * ldb;
 #pragma unroll
     for (int q = 0; q < Shape::QB; q++) {
       const bool ok = b_col_ok && (k0 + b_kk + Shape::B_KSTEP * q < K);
-      cp_async_elem<sizeof(T)>(bs + 2 * SBN * q, ok ? pb + q * b_qstep : b, ok);
+      cp_async_elem<sizeof(T)>(bs + Shape::B_KSTEP * BN * q,
+                               ok ? pb + q * b_qstep : b, ok);
     }
   };
 
@@ -218,94 +221,65 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
     const int64_t krem = K - kt * BK;
     const int kend = krem < BK ? (int)krem : BK;
 
-    if constexpr (MODEK >= 1) {
-      if constexpr (sizeof(T) == 4) {
-        auto fast_tile = [&](auto intfold) {
-          constexpr bool INTFOLD = decltype(intfold)::value;
-          auto fast_pair = [&](int kp) {
-            KPair<float> ap[8], bp[8];
-            const float4* pa4 = reinterpret_cast<const float4*>(as + kp * SBM + ty * 8);
+    if constexpr (MODEK >= 1 && sizeof(T) == 4) {
+      constexpr bool INTFOLD = MODEK == 2;
+      auto fast_pair = [&](int kp) {
+        KPair<float> ap[TM], bp[TN];
+        const float4* pa4 = reinterpret_cast<const float4*>(as + kp * BM + ty * TM);
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-              const float4 v = pa4[q];
-              ap[2 * q] = KPair<float>{v.x, v.y};
-              ap[2 * q + 1] = KPair<float>{v.z, v.w};
-            }
+        for (int q = 0; q < TM / 2; q++) {
+          const float4 v = pa4[q];
+          ap[2 * q] = KPair<float>{v.x, v.y};
+          ap[2 * q + 1] = KPair<float>{v.z, v.w};
+        }
 #pragma unroll
-            for (int g = 0; g < 4; g++) {
-              const float4 v = *reinterpret_cast<const float4*>(bs + kp * SBN + 32 * g + 2 * tx);
-              bp[2 * g] = KPair<float>{v.x, v.y};
-              bp[2 * g + 1] = KPair<float>{v.z, v.w};
-            }
-            if constexpr (LOOP == 0) {
+        for (int g = 0; g < TN / 2; g++) {
+          const float4 v = *reinterpret_cast<const float4*>(bs + kp * BN + 32 * g + 2 * tx);
+          bp[2 * g] = KPair<float>{v.x, v.y};
+          bp[2 * g + 1] = KPair<float>{v.z, v.w};
+        }
 #pragma unroll
-              for (int i = 0; i < 8; i++)
+        for (int i = 0; i < TM; i++)
 #pragma unroll
-                for (int j = 0; j < 8; j++) {
-                  float s0, s1;
-                  pair_combine<C>(ap[i], bp[j], s0, s1);
-                  acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
-                }
-            } else if constexpr (LOOP == 2) {
-#pragma unroll
-              for (int j = 0; j < 8; j++)
-#pragma unroll
-                for (int i = 0; i < 8; i++) {
-                  float s0, s1;
-                  pair_combine<C>(ap[i], bp[j], s0, s1);
-                  acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
-                }
-            } else {
-              constexpr int BATCH = LOOP == 1 ? 8 : 4;
-#pragma unroll
-              for (int i = 0; i < 8; i++)
-#pragma unroll
-                for (int j0 = 0; j0 < 8; j0 += BATCH) {
-                  float s0[BATCH], s1[BATCH];
-#pragma unroll
-                  for (int j = 0; j < BATCH; j++) pair_combine<C>(ap[i], bp[j0 + j], s0[j], s1[j]);
-#pragma unroll
-                  for (int j = 0; j < BATCH; j++)
-                    acc[i][j0 + j] = fold3<R, INTFOLD>(acc[i][j0 + j], s0[j], s1[j]);
-                }
-            }
-          };
-          if (kend == BK) {
-#pragma unroll
-            for (int kp = 0; kp < KP; kp++) fast_pair(kp);
-          } else {
-            for (int kp = 0; kp < kend / 2; kp++) fast_pair(kp);
-            if (kend & 1) {  // lone last k: one scalar combine + 2-input min/max
-              const int kp = kend / 2;
-              float av[8], bv[8];
-#pragma unroll
-              for (int i = 0; i < 8; i++) av[i] = as[kp * SBM + ty * 8 + i].x;
-#pragma unroll
-              for (int j = 0; j < 8; j++) bv[j] = bs[kp * SBN + 32 * (j >> 1) + 2 * tx + (j & 1)].x;
-#pragma unroll
-              for (int i = 0; i < 8; i++)
-#pragma unroll
-                for (int j = 0; j < 8; j++)
-                  acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
-            }
+          for (int j = 0; j < TN; j++) {
+            float s0, s1;
+            pair_combine<C>(ap[i], bp[j], s0, s1);
+            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
           }
-        };
-        fast_tile(std::integral_constant<bool, MODEK == 2>{});
+      };
+      if (kend == BK) {
+#pragma unroll
+        for (int kp = 0; kp < KP; kp++) fast_pair(kp);
+      } else {
+        for (int kp = 0; kp < kend / 2; kp++) fast_pair(kp);
+        if (kend & 1) {  // lone last k: one scalar combine + 2-input min/max
+          const int kp = kend / 2;
+          float av[TM], bv[TN];
+#pragma unroll
+          for (int i = 0; i < TM; i++) av[i] = as[kp * BM + ty * TM + i].x;
+#pragma unroll
+          for (int j = 0; j < TN; j++) bv[j] = bs[kp * BN + 32 * (j >> 1) + 2 * tx + (j & 1)].x;
+#pragma unroll
+          for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < TN; j++)
+              acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
+        }
       }
     } else {
       // exact loop: the reference's fold, k ascending, k beyond K skipped
       for (int kk = 0; kk < kend; kk++) {
-        const T* ak = reinterpret_cast<const T*>(as + (kk >> 1) * SBM + ty * 8) + (kk & 1);
-        const T* bk = reinterpret_cast<const T*>(bs + (kk >> 1) * SBN + 2 * tx) + (kk & 1);
-        A av[8], bv[8];
+        const T* ak = reinterpret_cast<const T*>(as + (kk >> 1) * BM + ty * TM) + (kk & 1);
+        const T* bk = reinterpret_cast<const T*>(bs + (kk >> 1) * BN + 2 * tx) + (kk & 1);
+        A av[TM], bv[TN];
 #pragma unroll
-        for (int i = 0; i < 8; i++) av[i] = A(ak[2 * i]);
+        for (int i = 0; i < TM; i++) av[i] = A(ak[2 * i]);
 #pragma unroll
-        for (int j = 0; j < 8; j++) bv[j] = A(bk[2 * (32 * (j >> 1) + (j & 1))]);
+        for (int j = 0; j < TN; j++) bv[j] = A(bk[2 * (32 * (j >> 1) + (j & 1))]);
 #pragma unroll
-        for (int i = 0; i < 8; i++)
+        for (int i = 0; i < TM; i++)
 #pragma unroll
-          for (int j = 0; j < 8; j++)
+          for (int j = 0; j < TN; j++)
             acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
       }
     }
@@ -314,11 +288,11 @@ __global__ void __launch_bounds__(SNT, (SemiringShape<T, R>::MIN_BLOCKS))
 
   // ---- epilogue ----
 #pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const int64_t row = m0 + ty * 8 + i;
+  for (int i = 0; i < TM; i++) {
+    const int64_t row = m0 + ty * TM + i;
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
+    for (int j = 0; j < TN; j++) {
       const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
       if (col < N) c[row * ldc + col] = convert<T, A>(acc[i][j]);
     }
@@ -360,13 +334,16 @@ void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* o
   count_launch();
 }
 
-template <typename T, int C, int R, bool ACC, int MODEK, int LOOP = MOA_SEMIRING_LOOP>
+template <typename T, int C, int R, bool ACC, int MODEK, int TM = DefaultTile<T, R>::TM,
+          int TN = DefaultTile<T, R>::TN, int MINB = DefaultTile<T, R>::MINB>
 cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
-  auto kern = semiring_kernel<T, C, R, ACC, MODEK, LOOP>;
-  const size_t smem = SemiringShape<T, R>::SMEM;
+  using Shape = SemiringShape<T, R, TM, TN, MINB>;
+  auto kern = semiring_kernel<T, C, R, ACC, MODEK, TM, TN, MINB>;
+  const size_t smem = Shape::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int64_t tiles_m = (p.M + SBM - 1) / SBM, tiles_n = (p.N + SBN - 1) / SBN;
+  const int64_t tiles_m = (p.M + Shape::BM - 1) / Shape::BM;
+  const int64_t tiles_n = (p.N + Shape::BN - 1) / Shape::BN;
   const int64_t tiles = tiles_m * tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   kern<<<(unsigned)tiles, SNT, smem, p.stream>>>(

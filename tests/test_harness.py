@@ -133,3 +133,41 @@ def test_product_command_matches_api(tmp_path, capsys):
     assert main(["product", "--mode", "inner", "--left", str(left), "--right", str(right),
                  "--combine", "add", "--reduce", "min", "--threads", "3", "--out", str(out)]) == 0
     assert moa.load(out).item() == 11.0
+
+
+def test_memory_failure_recorded_and_sweep_continues(monkeypatch):
+    """reference tests/test_bench.py: a size that runs out of memory becomes a
+    SizeFailure and the sweep goes on (the product itself stubbed: CPU test)."""
+    real = harness.operand_pair
+
+    def flaky(seed, rows, ell, n):
+        if n == 8:
+            raise MemoryError("simulated allocation failure")
+        return real(seed, rows, ell, n)
+
+    def fake_timer(config, a, b, n, out):
+        out.records.append(TimingRecord(config.mode, config.workers, config.ell, n, 0, 1e-3, 0.0))
+
+    monkeypatch.setattr(harness, "operand_pair", flaky)
+    monkeypatch.setattr(harness, "_time_product", fake_timer)
+    cfg = ExperimentConfig(mode="moa-inner", workers=1, ell=8, n_list=[4, 8, 16], repeats=1)
+    result = harness.run_experiment(cfg)
+    assert [r.n for r in result.records] == [4, 16]
+    assert len(result.failures) == 1 and result.failures[0].n == 8
+    assert "MemoryError" in result.failures[0].error
+    with pytest.raises(ValueError):
+        harness.run_experiment(ExperimentConfig(mode="moa-inner", rows=0))
+
+
+@pytest.mark.gpu
+def test_experiment_checksums_independent_of_workers_and_reproducible():
+    sums = {}
+    for workers in (1, 2, 4):
+        cfg = ExperimentConfig(mode="moa-inner", workers=workers, ell=16, n_list=[8], repeats=1,
+                               seed=3, rows=2)
+        sums[workers] = harness.run_experiment(cfg).records[0].checksum
+    assert sums[1] == sums[2] == sums[4]
+    cfg = ExperimentConfig(mode="moa-inner", workers=2, ell=8, n_list=[4], repeats=2, seed=5, rows=3)
+    r1, r2 = harness.run_experiment(cfg), harness.run_experiment(cfg)
+    assert [r.checksum for r in r1.records] == [r.checksum for r in r2.records]
+    assert all(r.threads == 2 and r.seconds > 0 for r in r1.records)

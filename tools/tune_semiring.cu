@@ -1,6 +1,6 @@
-// Instruction-order sweep for the float32 tropical fast loop at BASELINE
-// config 5's shape (tools; not part of the library).  Times each LOOP variant
-// of semiring_kernel and checks that all give identical bits.
+// Register-tile sweep for the float32 tropical fast loop (VIMNMX3 mode) at BASELINE
+// config 5's shape (tools; not part of the library).  Times each thread-tile
+// shape of semiring_kernel and checks that all give identical bits.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        -o tools/tune_semiring tools/tune_semiring.cu
 #include "../paper_0907_0792_b200/csrc/semiring.cu"
@@ -27,18 +27,18 @@ __global__ void count_diff(const float* a, const float* b, size_t n, unsigned lo
   atomicAdd(out, c);
 }
 
-template <int LOOP>
+template <int TM, int TN, int MINB>
 void trial(const moa::Problem& p0, float* out, float* ref, unsigned* special, unsigned long long* cnt) {
   moa::Problem p = p0;
   p.c = out;
   cudaEvent_t s, e;
   CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
-  CK((moa::semiring_launch<float, 0, 2, false, 2, LOOP>(p, special)));
+  CK((moa::semiring_launch<float, 0, 2, false, 2, TM, TN, MINB>(p, special)));
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < 2; r++) {
     CK(cudaEventRecord(s));
-    CK((moa::semiring_launch<float, 0, 2, false, 2, LOOP>(p, special)));
+    CK((moa::semiring_launch<float, 0, 2, false, 2, TM, TN, MINB>(p, special)));
     CK(cudaEventRecord(e)); CK(cudaEventSynchronize(e));
     float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
   }
@@ -49,8 +49,8 @@ void trial(const moa::Problem& p0, float* out, float* ref, unsigned* special, un
     CK(cudaMemcpy(&diff, cnt, 8, cudaMemcpyDeviceToHost));
   }
   const double pairs = (double)p.M * p.N * p.K;
-  printf("{\"loop\": %d, \"ms\": %.3f, \"Gpairs_s\": %.1f, \"frac_of_24475\": %.4f, \"bit_diffs\": %llu}\n",
-         LOOP, best, pairs / (best * 1e-3) / 1e9, pairs / (best * 1e-3) / 1e9 / 24475.4, diff);
+  printf("{\"tile\": \"%dx%d_%dcta\", \"ms\": %.3f, \"Gpairs_s\": %.1f, \"frac_of_24475\": %.4f, \"bit_diffs\": %llu}\n",
+         TM, TN, MINB, best, pairs / (best * 1e-3) / 1e9, pairs / (best * 1e-3) / 1e9 / 24475.4, diff);
   fflush(stdout);
 }
 
@@ -66,9 +66,12 @@ int main() {
   unsigned flags[2] = {moa::S_PINF | moa::S_PZERO, moa::S_PINF | moa::S_PZERO};  // mode 2 data
   CK(cudaMemcpy(special, flags, 8, cudaMemcpyHostToDevice));
   moa::Problem p{MOA_DTYPE_F32, ref, a, b, n, n, n, n, n, n, 0, 2, false, 0};
-  trial<0>(p, ref, ref, special, cnt);
-  trial<1>(p, c, ref, special, cnt);
-  trial<2>(p, c, ref, special, cnt);
-  trial<3>(p, c, ref, special, cnt);
+  trial<8, 8, 2>(p, ref, ref, special, cnt);
+  trial<4, 8, 3>(p, c, ref, special, cnt);
+  trial<8, 4, 3>(p, c, ref, special, cnt);
+  trial<4, 8, 2>(p, c, ref, special, cnt);
+  trial<4, 4, 4>(p, c, ref, special, cnt);
+  trial<16, 8, 1>(p, c, ref, special, cnt);
+  trial<8, 8, 1>(p, c, ref, special, cnt);
   return 0;
 }
