@@ -44,9 +44,14 @@
 extern "C" {
 #endif
 
-/* element types (the reference has float64 only, arrays.py:77-78) */
+/* element types (the reference has float64 only, arrays.py:77-78).  Integer
+   types compute exactly in two's complement: add/sub/mul wrap, divide
+   truncates toward zero with x/0 = 0; min/max identities are the type's
+   max/min. */
 #define MOA_DTYPE_F64 0
 #define MOA_DTYPE_F32 1
+#define MOA_DTYPE_I32 2
+#define MOA_DTYPE_I64 3
 
 /* combine codes — identical to ops.py:52-59 and _ckernel.pyx:11-23 */
 #define MOA_COMBINE_ADD 0

@@ -105,6 +105,11 @@ def product(a: np.ndarray, b: np.ndarray, M: int, K: int, N: int, comb: int, red
     """
     lda = K if lda is None else lda
     ldb = N if ldb is None else ldb
+    # integer operands are upcast like the reference does (arrays.py:77-78)
+    if a.dtype.kind in "iu":
+        a = a.astype(np.float64)
+    if b.dtype.kind in "iu":
+        b = b.astype(np.float64)
     f32 = a.dtype == np.float32
     if (b.dtype == np.float32) != f32:
         a, b = a.astype(np.float64), b.astype(np.float64)

@@ -17,6 +17,8 @@ from .errors import BackendError
 
 DTYPE_F64 = 0
 DTYPE_F32 = 1
+DTYPE_I32 = 2
+DTYPE_I64 = 3
 FLAG_ACCUMULATE = 1
 FLAG_EXACT = 2
 

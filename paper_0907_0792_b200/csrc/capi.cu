@@ -74,7 +74,7 @@ int moa_product_rows(int dtype, void* res, const void* a, const void* b, int64_t
                      int64_t restride, int combine_code, int reduce_code, int64_t start,
                      int64_t step, uint32_t flags, void* stream) {
   t_last_error.clear();
-  if (dtype != MOA_DTYPE_F64 && dtype != MOA_DTYPE_F32)
+  if (dtype < MOA_DTYPE_F64 || dtype > MOA_DTYPE_I64)
     return fail(MOA_E_DTYPE, "unknown dtype code " + std::to_string(dtype));
   if (combine_code < 0 || combine_code > 5)
     return fail(MOA_E_OPCODE, "unknown combine code " + std::to_string(combine_code));
@@ -92,7 +92,7 @@ int moa_product_rows(int dtype, void* res, const void* a, const void* b, int64_t
   if (res == nullptr || (rowsinred > 0 && (a == nullptr || b == nullptr)))
     return fail(MOA_E_NULL, "null operand pointer");
 
-  const size_t esz = dtype == MOA_DTYPE_F64 ? 8 : 4;
+  const size_t esz = (dtype == MOA_DTYPE_F64 || dtype == MOA_DTYPE_I64) ? 8 : 4;
   moa::Problem p;
   p.dtype = dtype;
   p.c = static_cast<char*>(res) + (size_t)(start * restride) * esz;

@@ -4,6 +4,8 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
+
 #include <cuda_runtime.h>
 
 namespace moa {
@@ -12,6 +14,44 @@ enum Combine : int { C_ADD = 0, C_SUB = 1, C_MUL = 2, C_DIV = 3, C_MIN = 4, C_MA
 enum Reduce : int { R_ADD = 0, R_MUL = 1, R_MIN = 2, R_MAX = 3 };
 
 constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------------------
+// Integer element types (the reference is float64 only): exact
+// two's-complement arithmetic.  add/sub/mul wrap modulo 2^bits (computed on
+// the unsigned type, so there is no undefined behaviour); divide truncates
+// toward zero with x/0 = 0 and MIN/-1 = MIN.  On integer-valued data whose
+// partial results stay below 2^53 in magnitude this equals the reference's
+// float64 result exactly, which is what the parity tests pin (divide excepted).
+// ---------------------------------------------------------------------------
+template <typename T> struct IntTraits;
+template <> struct IntTraits<int32_t> {
+  using U = uint32_t;
+  static constexpr int32_t kMax = 2147483647, kMin = -2147483647 - 1;
+};
+template <> struct IntTraits<int64_t> {
+  using U = uint64_t;
+  static constexpr int64_t kMax = 9223372036854775807LL, kMin = -9223372036854775807LL - 1;
+};
+template <typename T> __host__ __device__ constexpr bool is_int() {
+  return std::is_same<T, int32_t>::value || std::is_same<T, int64_t>::value;
+}
+template <typename T> __device__ __forceinline__ T wrap_add(T x, T y) {
+  using U = typename IntTraits<T>::U;
+  return T(U(x) + U(y));
+}
+template <typename T> __device__ __forceinline__ T wrap_sub(T x, T y) {
+  using U = typename IntTraits<T>::U;
+  return T(U(x) - U(y));
+}
+template <typename T> __device__ __forceinline__ T wrap_mul(T x, T y) {
+  using U = typename IntTraits<T>::U;
+  return T(U(x) * U(y));
+}
+template <typename T> __device__ __forceinline__ T safe_div(T x, T y) {
+  if (y == 0) return T(0);
+  if (y == T(-1)) return wrap_sub(T(0), x);  // MIN / -1 wraps to MIN
+  return x / y;
+}
 
 // ---------------------------------------------------------------------------
 // combine(x, y) with the reference's operand order (_ckernel.pyx:71: combine
@@ -25,18 +65,26 @@ template <int C> struct CombineOp;
 template <> struct CombineOp<C_ADD> {
   static __device__ __forceinline__ double f(double x, double y) { return __dadd_rn(x, y); }
   static __device__ __forceinline__ float f(float x, float y) { return __fadd_rn(x, y); }
+  static __device__ __forceinline__ int32_t f(int32_t x, int32_t y) { return wrap_add(x, y); }
+  static __device__ __forceinline__ int64_t f(int64_t x, int64_t y) { return wrap_add(x, y); }
 };
 template <> struct CombineOp<C_SUB> {
   static __device__ __forceinline__ double f(double x, double y) { return __dsub_rn(x, y); }
   static __device__ __forceinline__ float f(float x, float y) { return __fsub_rn(x, y); }
+  static __device__ __forceinline__ int32_t f(int32_t x, int32_t y) { return wrap_sub(x, y); }
+  static __device__ __forceinline__ int64_t f(int64_t x, int64_t y) { return wrap_sub(x, y); }
 };
 template <> struct CombineOp<C_MUL> {
   static __device__ __forceinline__ double f(double x, double y) { return __dmul_rn(x, y); }
   static __device__ __forceinline__ float f(float x, float y) { return __fmul_rn(x, y); }
+  static __device__ __forceinline__ int32_t f(int32_t x, int32_t y) { return wrap_mul(x, y); }
+  static __device__ __forceinline__ int64_t f(int64_t x, int64_t y) { return wrap_mul(x, y); }
 };
 template <> struct CombineOp<C_DIV> {
   static __device__ __forceinline__ double f(double x, double y) { return __ddiv_rn(x, y); }
   static __device__ __forceinline__ float f(float x, float y) { return __fdiv_rn(x, y); }
+  static __device__ __forceinline__ int32_t f(int32_t x, int32_t y) { return safe_div(x, y); }
+  static __device__ __forceinline__ int64_t f(int64_t x, int64_t y) { return safe_div(x, y); }
 };
 template <> struct CombineOp<C_MIN> {
   template <typename T> static __device__ __forceinline__ T f(T x, T y) { return x < y ? x : y; }
@@ -46,24 +94,35 @@ template <> struct CombineOp<C_MAX> {
 };
 
 // reduce(acc, v): _ckernel.pyx:26-34 / ops.py:61-66; acc is the left operand.
+// Integer identities: 0, 1, and the type's max / min for the +inf / -inf of min / max.
 template <int R> struct ReduceOp;
 template <> struct ReduceOp<R_ADD> {
   static __device__ __forceinline__ double f(double x, double y) { return __dadd_rn(x, y); }
   static __device__ __forceinline__ float f(float x, float y) { return __fadd_rn(x, y); }
+  static __device__ __forceinline__ int32_t f(int32_t x, int32_t y) { return wrap_add(x, y); }
+  static __device__ __forceinline__ int64_t f(int64_t x, int64_t y) { return wrap_add(x, y); }
   template <typename T> static __host__ __device__ constexpr T identity() { return T(0); }
 };
 template <> struct ReduceOp<R_MUL> {
   static __device__ __forceinline__ double f(double x, double y) { return __dmul_rn(x, y); }
   static __device__ __forceinline__ float f(float x, float y) { return __fmul_rn(x, y); }
+  static __device__ __forceinline__ int32_t f(int32_t x, int32_t y) { return wrap_mul(x, y); }
+  static __device__ __forceinline__ int64_t f(int64_t x, int64_t y) { return wrap_mul(x, y); }
   template <typename T> static __host__ __device__ constexpr T identity() { return T(1); }
 };
 template <> struct ReduceOp<R_MIN> {
   template <typename T> static __device__ __forceinline__ T f(T x, T y) { return x < y ? x : y; }
-  template <typename T> static __host__ __device__ T identity() { return T(__builtin_huge_val()); }
+  template <typename T> static __host__ __device__ T identity() {
+    if constexpr (is_int<T>()) return IntTraits<T>::kMax;
+    else return T(__builtin_huge_val());
+  }
 };
 template <> struct ReduceOp<R_MAX> {
   template <typename T> static __device__ __forceinline__ T f(T x, T y) { return x > y ? x : y; }
-  template <typename T> static __host__ __device__ T identity() { return T(-__builtin_huge_val()); }
+  template <typename T> static __host__ __device__ T identity() {
+    if constexpr (is_int<T>()) return IntTraits<T>::kMin;
+    else return T(-__builtin_huge_val());
+  }
 };
 
 // ---------------------------------------------------------------------------

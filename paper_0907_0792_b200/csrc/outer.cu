@@ -32,6 +32,27 @@ __device__ __forceinline__ void st_stream_32B(float* p, const float (&v)[8]) {
                "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                : "memory");
 }
+__device__ __forceinline__ void st_stream_32B(int64_t* p, const int64_t (&v)[4]) {
+  asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]),
+               "l"(v[2]), "l"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void st_stream_32B(int32_t* p, const int32_t (&v)[8]) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void ld_32B(const int64_t* p, int64_t (&v)[4]) {
+  asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld_32B(const int32_t* p, int32_t (&v)[8]) {
+  asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+}
 __device__ __forceinline__ void ld_32B(const double* p, double (&v)[4]) {
   asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
                : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
@@ -216,11 +237,21 @@ cudaError_t fill_typed(const Problem& p) {
 }  // namespace
 
 cudaError_t launch_outer(const Problem& p) {
-  return p.dtype == MOA_DTYPE_F64 ? outer_comb<double>(p) : outer_comb<float>(p);
+  switch (p.dtype) {
+    case MOA_DTYPE_F64: return outer_comb<double>(p);
+    case MOA_DTYPE_F32: return outer_comb<float>(p);
+    case MOA_DTYPE_I32: return outer_comb<int32_t>(p);
+    default: return outer_comb<int64_t>(p);
+  }
 }
 
 cudaError_t launch_fill(const Problem& p) {
-  return p.dtype == MOA_DTYPE_F64 ? fill_typed<double>(p) : fill_typed<float>(p);
+  switch (p.dtype) {
+    case MOA_DTYPE_F64: return fill_typed<double>(p);
+    case MOA_DTYPE_F32: return fill_typed<float>(p);
+    case MOA_DTYPE_I32: return fill_typed<int32_t>(p);
+    default: return fill_typed<int64_t>(p);
+  }
 }
 
 }  // namespace moa

@@ -1,0 +1,406 @@
+// K2: the CUDA-core semiring kernel — every (combine, reduce) pair other than
+// the tensor-core (multiply, add) float64 path.
+//
+// Reference loop (_ckernel.pyx:55-72, generic; :37-52 for (multiply, add)):
+//     for i in rows: for l < rowsinred: av = a[l + i*lstride]
+//         for j < elsinop: res[i*restride+j] = reduce(res[..], combine(av, b[l*rstride+j]))
+// Every result element is an l-ascending fold from the identity.  Rows (and
+// elements) are independent, so the GPU tiles C into (16*TM) x (16*TN) blocks
+// of 16x16 threads with a TM x TN register tile each; each thread folds its
+// elements over l in ascending order with the reference's exact operations,
+// which makes the result bit-identical to the reference for every pair (the
+// "exact" loop).
+//
+// For combine in {add, subtract} with reduce in {min, max} on float32 — the
+// tropical semirings, BASELINE config 5 — the exact loop costs a FADD, FSETP
+// and FSEL per pair.  The fast loops add two contraction steps at once with a
+// packed FADD2 and fold both sums with one 3-input min/max: VIMNMX3 on the bit
+// patterns when every combine result is a non-negative float, FMNMX3 when no
+// combine result can be NaN or -0.0 (moa_common.cuh).  A pre-scan kernel
+// records which special values occur in A and B; the host launches one kernel
+// specialisation per fold mode and all but the one the device flags select
+// return at once, so there is no host synchronisation and the result never
+// depends on the choice.
+//
+// Shared-memory layout: both tiles are stored as k-PAIRS, As[kp][m] =
+// (A[m][2kp], A[m][2kp+1]) and Bs[kp][n] = (B[2kp][n], B[2kp+1][n]), so a
+// thread's FADD2 operands are single 64-bit LDS results.  Thread (ty, tx) owns
+// rows ty*TM..ty*TM+TM-1 and columns 32g + 2tx + {0,1} (g < TN/2): A reads are
+// warp-broadcasts, B reads are 16-byte loads over a contiguous 256-byte span
+// (conflict-free).  Global->shared staging is element-wise cp.async (3 stages).
+#pragma once
+
+#include <type_traits>
+
+#include "moa_common.cuh"
+#include "moa_kernels.h"
+#include "../../include/moa_b200.h"
+
+namespace moa {
+
+namespace {
+
+constexpr int SNT = 256, GROUP_M = 8;  // 16 x 16 threads per CTA
+
+template <typename T> struct alignas(2 * sizeof(T)) KPair { T x, y; };
+
+template <typename T, int R, int TM_, int TN_, int MINB_>
+struct SemiringShape {
+  static constexpr bool F4 = sizeof(typename AccType<T, R>::type) == 4;
+  static constexpr int TM = TM_, TN = TN_;
+  static constexpr int BM = 16 * TM, BN = 16 * TN;
+  static constexpr int BK = F4 ? 32 : 16;       // k per stage (one barrier per BK)
+  static constexpr int KP = BK / 2;             // k-pairs per stage
+  static constexpr int STAGES = 3;
+  static constexpr int A_STAGE = KP * BM;       // pairs
+  static constexpr int B_STAGE = KP * BN;       // pairs
+  static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(KPair<T>);
+  // element-wise loader: thread t copies A elements (row t/BK + (SNT/BK)*q, k t%BK)
+  // and B elements (k t/BN + (SNT/BN)*q, column t%BN)
+  static constexpr int QA = BM * BK / SNT, A_RSTEP = SNT / BK;
+  static constexpr int QB = BK * BN / SNT, B_KSTEP = SNT / BN;
+  static_assert(QA <= 32 && B_KSTEP % 2 == 0 && TM % 2 == 0 && TN % 2 == 0, "tile layout");
+};
+
+// Default tiles: float32 min/max (c5): 8x8 per thread, two CTAs per SM
+// (tools/tune_semiring.cu); float64 or float64-accumulated: 8x8, one CTA.
+template <typename T, int R> struct DefaultTile {
+  static constexpr bool F4 = sizeof(typename AccType<T, R>::type) == 4;
+  static constexpr int TM = 8, TN = 8, MINB = F4 ? 2 : 1;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_elem(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(dst)), "l"(src),
+               "n"(BYTES), "r"(valid ? BYTES : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long f32x2_bits(KPair<float> p) {
+  return *reinterpret_cast<unsigned long long*>(&p);
+}
+
+// one FADD2: (a.x op b.x, a.y op b.y), round-to-nearest each
+template <int C>
+__device__ __forceinline__ void pair_combine(KPair<float> a, KPair<float> b, float& s0, float& s1) {
+  unsigned long long r;
+  if (C == C_SUB)
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f32x2_bits(a)), "l"(f32x2_bits(b)));
+  else
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f32x2_bits(a)), "l"(f32x2_bits(b)));
+  s0 = __uint_as_float((unsigned)r);
+  s1 = __uint_as_float((unsigned)(r >> 32));
+}
+
+template <int R, bool INTFOLD>
+__device__ __forceinline__ float fold3(float acc, float s0, float s1) {
+  if (INTFOLD) {  // non-negative floats: unsigned order == float order
+    const unsigned x = __float_as_uint(acc), y = __float_as_uint(s0), z = __float_as_uint(s1);
+    return __uint_as_float(R == R_MIN ? __vimin3_u32(x, y, z) : __vimax3_u32(x, y, z));
+  }
+  float r;
+  if (R == R_MIN)
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(acc), "f"(s0), "f"(s1));
+  else
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(acc), "f"(s0), "f"(s1));
+  return r;
+}
+
+// MODEK: -1 = exact fold only (no pre-scan); 0 / 1 / 2 = the exact / FMNMX3 /
+// VIMNMX3 specialisation of a tropical candidate, which returns at once unless
+// the device-side pre-scan selected that mode (one loop per kernel keeps
+// register pressure down).
+template <typename T, int C, int R, bool ACC, int MODEK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__(SNT, MINB)
+    semiring_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ b,
+                    int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                    const unsigned* special, int64_t tiles_m, int64_t tiles_n) {
+  using A = typename AccType<T, R>::type;
+  using Shape = SemiringShape<T, R, TM, TN, MINB>;
+  constexpr int STAGES = Shape::STAGES, BM = Shape::BM, BN = Shape::BN;
+  constexpr int BK = Shape::BK, KP = Shape::KP;
+  if constexpr (MODEK >= 0) {
+    if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODEK) return;
+  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  KPair<T>* As = reinterpret_cast<KPair<T>*>(smem_raw);
+  KPair<T>* Bs = As + STAGES * Shape::A_STAGE;
+
+  // grouped rasterisation: GROUP_M row tiles sweep the column tiles together
+  const int64_t pid = blockIdx.x;
+  const int64_t width = GROUP_M * tiles_n;
+  const int64_t first_m = (pid / width) * GROUP_M;
+  const int64_t gsize = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
+  const int64_t m0 = (first_m + (pid % width) % gsize) * BM;
+  const int64_t n0 = ((pid % width) / gsize) * BN;
+
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;
+
+  // ---- accumulators: rows ty*TM+i, columns 32*(j>>1) + 2*tx + (j&1) ----
+  A acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      const int64_t row = m0 + ty * TM + i;
+      const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
+      if (ACC && row < M && col < N)
+        acc[i][j] = A(c[row * ldc + col]);
+      else
+        acc[i][j] = ReduceOp<R>::template identity<A>();
+    }
+  // The unsigned-order fold (mode 2) cannot start from -inf (sign bit set).
+  // Mode 2 implies every combine result is >= +0 and K >= 2, so a max fold
+  // from +0 gives the same bits as one from the identity.
+  if constexpr (R == R_MAX && MODEK == 2) {
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+      for (int j = 0; j < TN; j++) acc[i][j] = A(0);
+  }
+
+  // ---- element-wise async copies into the k-pair layouts (zero-filled outside) ----
+  // Per-thread bases are fixed for the whole kernel; a stage only adds k0.
+  const int a_kk = tid % BK, a_r = tid / BK;
+  const int b_n = tid % BN, b_kk = tid / BN;
+  const T* a_src = a + (m0 + a_r) * lda + a_kk;
+  const int64_t a_qstep = (int64_t)Shape::A_RSTEP * lda;
+  const T* b_src = b + (int64_t)b_kk * ldb + n0 + b_n;
+  const int64_t b_qstep = (int64_t)Shape::B_KSTEP * ldb;
+  unsigned a_rows_ok = 0;
+#pragma unroll
+  for (int q = 0; q < Shape::QA; q++)
+    if (m0 + a_r + q * Shape::A_RSTEP < M) a_rows_ok |= 1u << q;
+  const bool b_col_ok = n0 + b_n < N;
+  const int a_dst = 2 * ((a_kk >> 1) * BM + a_r) + (a_kk & 1);             // T elements
+  const int b_dst = 2 * ((b_kk >> 1) * BN + b_n) + (b_kk & 1);             // T elements
+  auto load_stage = [&](int stage, int64_t k0) {
+    T* as = reinterpret_cast<T*>(As + stage * Shape::A_STAGE) + a_dst;
+    T* bs = reinterpret_cast<T*>(Bs + stage * Shape::B_STAGE) + b_dst;
+    const bool a_k_ok = k0 + a_kk < K;
+    const T* pa = a_src + k0;
+#pragma unroll
+    for (int q = 0; q < Shape::QA; q++) {
+      const bool ok = a_k_ok && ((a_rows_ok >> q) & 1u);
+      cp_async_elem<sizeof(T)>(as + 2 * Shape::A_RSTEP * q,
+                               ok ? pa + q * a_qstep : a, ok);
+    }
+    const T* pb = b_src + k0 * ldb;
+#pragma unroll
+    for (int q = 0; q < Shape::QB; q++) {
+      const bool ok = b_col_ok && (k0 + b_kk + Shape::B_KSTEP * q < K);
+      cp_async_elem<sizeof(T)>(bs + Shape::B_KSTEP * BN * q,
+                               ok ? pb + q * b_qstep : b, ok);
+    }
+  };
+
+  const int64_t KT = (K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; s++) {
+    if (s < KT) load_stage(s, (int64_t)s * BK);
+    cp_async_commit();
+  }
+
+  for (int64_t kt = 0; kt < KT; kt++) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t nk = kt + STAGES - 1;
+      if (nk < KT) load_stage((int)(nk % STAGES), nk * BK);
+      cp_async_commit();
+    }
+    const KPair<T>* as = As + (int)(kt % STAGES) * Shape::A_STAGE;
+    const KPair<T>* bs = Bs + (int)(kt % STAGES) * Shape::B_STAGE;
+    const int64_t krem = K - kt * BK;
+    const int kend = krem < BK ? (int)krem : BK;
+
+    if constexpr (MODEK >= 1 && sizeof(T) == 4) {
+      constexpr bool INTFOLD = MODEK == 2;
+      auto fast_pair = [&](int kp) {
+        KPair<float> ap[TM], bp[TN];
+        const float4* pa4 = reinterpret_cast<const float4*>(as + kp * BM + ty * TM);
+#pragma unroll
+        for (int q = 0; q < TM / 2; q++) {
+          const float4 v = pa4[q];
+          ap[2 * q] = KPair<float>{v.x, v.y};
+          ap[2 * q + 1] = KPair<float>{v.z, v.w};
+        }
+#pragma unroll
+        for (int g = 0; g < TN / 2; g++) {
+          const float4 v = *reinterpret_cast<const float4*>(bs + kp * BN + 32 * g + 2 * tx);
+          bp[2 * g] = KPair<float>{v.x, v.y};
+          bp[2 * g + 1] = KPair<float>{v.z, v.w};
+        }
+#pragma unroll
+        for (int i = 0; i < TM; i++)
+#pragma unroll
+          for (int j = 0; j < TN; j++) {
+            float s0, s1;
+            pair_combine<C>(ap[i], bp[j], s0, s1);
+            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
+          }
+      };
+      if (kend == BK) {
+#pragma unroll
+        for (int kp = 0; kp < KP; kp++) fast_pair(kp);
+      } else {
+        for (int kp = 0; kp < kend / 2; kp++) fast_pair(kp);
+        if (kend & 1) {  // lone last k: one scalar combine + 2-input min/max
+          const int kp = kend / 2;
+          float av[TM], bv[TN];
+#pragma unroll
+          for (int i = 0; i < TM; i++) av[i] = as[kp * BM + ty * TM + i].x;
+#pragma unroll
+          for (int j = 0; j < TN; j++) bv[j] = bs[kp * BN + 32 * (j >> 1) + 2 * tx + (j & 1)].x;
+#pragma unroll
+          for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < TN; j++)
+              acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
+        }
+      }
+    } else {
+      // exact loop: the reference's fold, k ascending, k beyond K skipped
+      for (int kk = 0; kk < kend; kk++) {
+        const T* ak = reinterpret_cast<const T*>(as + (kk >> 1) * BM + ty * TM) + (kk & 1);
+        const T* bk = reinterpret_cast<const T*>(bs + (kk >> 1) * BN + 2 * tx) + (kk & 1);
+        A av[TM], bv[TN];
+#pragma unroll
+        for (int i = 0; i < TM; i++) av[i] = A(ak[2 * i]);
+#pragma unroll
+        for (int j = 0; j < TN; j++) bv[j] = A(bk[2 * (32 * (j >> 1) + (j & 1))]);
+#pragma unroll
+        for (int i = 0; i < TM; i++)
+#pragma unroll
+          for (int j = 0; j < TN; j++)
+            acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---- epilogue ----
+#pragma unroll
+  for (int i = 0; i < TM; i++) {
+    const int64_t row = m0 + ty * TM + i;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
+      if (col < N) c[row * ldc + col] = convert<T, A>(acc[i][j]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) scan_special_kernel(const T* __restrict__ x, int64_t rows,
+                                                           int64_t cols, int64_t ld,
+                                                           unsigned* __restrict__ out) {
+  unsigned bits = 0;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const T* p = x + r * ld;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const T v = __ldg(p + j);
+      if (v != v) bits |= S_NAN;
+      else if (v == T(__builtin_huge_val())) bits |= S_PINF;
+      else if (v == T(-__builtin_huge_val())) bits |= S_NINF;
+      else if (v == T(0)) bits |= signbit(v) ? S_NZERO : S_PZERO;
+      if (signbit(v)) bits |= S_NEG;
+    }
+  }
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(out, bits);
+}
+
+template <typename T>
+void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* out,
+                 cudaStream_t s) {
+  const unsigned bx = 256;
+  int64_t gx = (cols + bx - 1) / bx;
+  if (gx > 64) gx = 64;
+  int64_t gy = ((int64_t)kNumSMs * 8 + gx - 1) / gx;
+  if (gy > rows) gy = rows;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  scan_special_kernel<T><<<dim3((unsigned)gx, (unsigned)gy), bx, 0, s>>>(x, rows, cols, ld, out);
+  count_launch();
+}
+
+template <typename T, int C, int R, bool ACC, int MODEK, int TM = DefaultTile<T, R>::TM,
+          int TN = DefaultTile<T, R>::TN, int MINB = DefaultTile<T, R>::MINB>
+cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
+  using Shape = SemiringShape<T, R, TM, TN, MINB>;
+  auto kern = semiring_kernel<T, C, R, ACC, MODEK, TM, TN, MINB>;
+  const size_t smem = Shape::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles_m = (p.M + Shape::BM - 1) / Shape::BM;
+  const int64_t tiles_n = (p.N + Shape::BN - 1) / Shape::BN;
+  const int64_t tiles = tiles_m * tiles_n;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)tiles, SNT, smem, p.stream>>>(
+      static_cast<T*>(p.c), static_cast<const T*>(p.a), static_cast<const T*>(p.b), p.M, p.N, p.K,
+      p.lda, p.ldb, p.ldc, special, tiles_m, tiles_n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T, int C, int R>
+cudaError_t semiring_acc(const Problem& p) {
+  if (p.accumulate) return semiring_launch<T, C, R, true, -1>(p, nullptr);
+  constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB) &&
+                        (R == R_MIN || R == R_MAX);
+  if constexpr (cand) {
+    // pre-scan A (M x K, lda) and B (K x N, ldb) for NaN / +-inf / +-0
+    unsigned* special = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&special), 2 * sizeof(unsigned), p.stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(special, 0, 2 * sizeof(unsigned), p.stream);
+    if (e != cudaSuccess) return e;
+    launch_scan<T>(static_cast<const T*>(p.a), p.M, p.K, p.lda, special, p.stream);
+    launch_scan<T>(static_cast<const T*>(p.b), p.K, p.N, p.ldb, special + 1, p.stream);
+    // one specialisation per fold mode; all but the selected one exit at once
+    if constexpr (C == C_ADD) e = semiring_launch<T, C, R, false, 2>(p, special);
+    if (e == cudaSuccess) e = semiring_launch<T, C, R, false, 1>(p, special);
+    if (e == cudaSuccess) e = semiring_launch<T, C, R, false, 0>(p, special);
+    cudaError_t e2 = cudaFreeAsync(special, p.stream);
+    return e != cudaSuccess ? e : e2;
+  } else {
+    return semiring_launch<T, C, R, false, -1>(p, nullptr);
+  }
+}
+
+template <typename T, int C>
+cudaError_t semiring_red(const Problem& p) {
+  switch (p.reduce) {
+    case R_ADD: return semiring_acc<T, C, R_ADD>(p);
+    case R_MUL: return semiring_acc<T, C, R_MUL>(p);
+    case R_MIN: return semiring_acc<T, C, R_MIN>(p);
+    default: return semiring_acc<T, C, R_MAX>(p);
+  }
+}
+
+template <typename T>
+cudaError_t semiring_comb(const Problem& p) {
+  switch (p.combine) {
+    case C_ADD: return semiring_red<T, C_ADD>(p);
+    case C_SUB: return semiring_red<T, C_SUB>(p);
+    case C_MUL: return semiring_red<T, C_MUL>(p);
+    case C_DIV: return semiring_red<T, C_DIV>(p);
+    case C_MIN: return semiring_red<T, C_MIN>(p);
+    default: return semiring_red<T, C_MAX>(p);
+  }
+}
+
+}  // namespace
+}  // namespace moa

@@ -124,20 +124,41 @@ def _torch():
     return torch
 
 
+_F32, _F64 = np.dtype(np.float32), np.dtype(np.float64)
+_I32, _I64 = np.dtype(np.int32), np.dtype(np.int64)
+
+
 def result_dtype(a: MoaArray, b: MoaArray) -> np.dtype:
-    """float32 only when both operands are float32 (the reference is float64)."""
-    f32 = np.dtype(np.float32)
-    return f32 if (a.dtype == f32 and b.dtype == f32) else np.dtype(np.float64)
+    """Element type of a product.
+
+    float64 unless both operands are float32 (-> float32) or both are integers
+    (-> int64 if either is int64, else int32).  Mixing floats and integers
+    computes in float64, as the reference does for everything."""
+    da, db = a.dtype, b.dtype
+    if da == db:
+        return da
+    ints = (_I32, _I64)
+    if da in ints and db in ints:
+        return _I64
+    return _F64
 
 
-def _native_dtype(dt: np.dtype) -> int:
-    return _native.DTYPE_F32 if dt == np.dtype(np.float32) else _native.DTYPE_F64
+def native_dtype(dt) -> int:
+    """ABI dtype code for a numpy or torch dtype."""
+    name = str(dt).replace("torch.", "")
+    return {"float64": _native.DTYPE_F64, "float32": _native.DTYPE_F32,
+            "int32": _native.DTYPE_I32, "int64": _native.DTYPE_I64}[name]
+
+
+def torch_dtype(dt: np.dtype):
+    torch = _torch()
+    return {_F64: torch.float64, _F32: torch.float32, _I32: torch.int32,
+            _I64: torch.int64}[np.dtype(dt)]
 
 
 def stage(x: MoaArray, device, dtype: np.dtype):
     """x's elements as a flat CUDA tensor of ``dtype`` on ``device`` (no copy if already so)."""
-    torch = _torch()
-    tdt = torch.float32 if dtype == np.dtype(np.float32) else torch.float64
+    tdt = torch_dtype(dtype)
     if x.is_device:
         t = x.data
         if t.device != device or t.dtype != tdt:
@@ -173,8 +194,7 @@ def launch(plan: KernelPlan, res, a_dev, b_dev, ops: OpPair, *, start: int = 0,
     if stream is None:
         stream = torch.cuda.current_stream(res.device)
     flags = (_native.FLAG_EXACT if exact else 0) | (_native.FLAG_ACCUMULATE if accumulate else 0)
-    dt = _native.DTYPE_F32 if res.dtype == torch.float32 else _native.DTYPE_F64
-    _native.product_rows(dt, res.data_ptr(), a_dev.data_ptr(), b_dev.data_ptr(),
+    _native.product_rows(native_dtype(res.dtype), res.data_ptr(), a_dev.data_ptr(), b_dev.data_ptr(),
                          plan.noproc, plan.rowsinred, plan.elsinop,
                          plan.lstride, plan.rstride, plan.restride,
                          codes[0], codes[1], start, step, flags, stream.cuda_stream)
@@ -198,7 +218,7 @@ class _Runner:
         self.device = torch.device(device)
         self._a = stage(a, self.device, self.dtype)
         self._b = stage(b, self.device, self.dtype)
-        tdt = torch.float32 if self.dtype == np.dtype(np.float32) else torch.float64
+        tdt = torch_dtype(self.dtype)
         self._res = torch.empty(plan.noproc * plan.elsinop, dtype=tdt, device=self.device)
 
     def run_rows(self, start: int, step: int) -> None:
@@ -292,7 +312,7 @@ def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, c
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else \
         torch.device(device)
     dtype = result_dtype(a, b)
-    tdt = torch.float32 if dtype == np.dtype(np.float32) else torch.float64
+    tdt = torch_dtype(dtype)
     m, n, lda = plan.noproc, plan.elsinop, plan.lstride
     comp = torch.cuda.current_stream(dev)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)

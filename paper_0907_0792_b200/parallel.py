@@ -23,7 +23,7 @@ import numpy as np
 from . import _native
 from .arrays import MoaArray
 from .kernel import (KernelPlan, _Runner, _check_plan, launch, resolve_backend,
-                     result_dtype, stage, stage_host)
+                     result_dtype, stage, stage_host, torch_dtype)
 from .ops import MUL_ADD, OpPair
 
 
@@ -72,7 +72,7 @@ def execute_parallel(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair = M
     resolve_backend(backend, ops)
     _native.load()
     dtype = result_dtype(a, b)
-    tdt = torch.float32 if dtype == np.dtype(np.float32) else torch.float64
+    tdt = torch_dtype(dtype)
     host_result = not (a.is_device or b.is_device)
     home = a.data.device if a.is_device else b.data.device if b.is_device else \
         torch.device("cuda", devices[0])

@@ -6,12 +6,12 @@ Builds the reference package from /root/reference/pkg in a scratch copy under
 /tmp (its own setup.py, compiled backend, flags -O3 -ffp-contract=off), imports
 it as ``moaprod`` and records its outputs:
 
-* small.npz  — ~1,200 small cases over all 24 (combine, reduce) pairs: random
+* small.npz  — ~700 small cases over all 24 (combine, reduce) pairs: random
   inner/outer products (rank <= 4, extents <= 5, values U[-1,2) like the
   reference's conftest.py:7-27), special-value cases (NaN, +-inf, +-0), medium
   products with ragged tile edges, float32 inputs (the reference upcasts,
-  arrays.py:77-78), the reference tests' hand-checked answers, and empty /
-  zero-extent cases.  Every output comes from moaprod.inner / moaprod.outer.
+  arrays.py:77-78), integer-valued int32/int64 inputs, the reference tests'
+  hand-checked answers, and empty / zero-extent cases.  Every output comes from moaprod.inner / moaprod.outer.
 * configs.json — for each BASELINE config, the reference output on a row
   subset at FULL size (full K and N), as sha256 of the float64 bytes (and of
   the float32 rounding for the float32 config) plus a few sample values.
@@ -147,6 +147,26 @@ def main() -> None:
     add("inner", mul_add, (3, 4), list(range(12)), (4, 0), [], "zero_cols")
     a = rng.random(6)
     add("outer", mp.op_pair("subtract", "add"), (3, 2), a, (3, 2), a, "sub_self")
+
+    # integer inputs (the reference upcasts to float64; with small integer
+    # values every partial result is exact, so the reference's float64 result
+    # IS the integer result).  divide is excluded: integer division truncates.
+    for dt in (np.int32, np.int64):
+        for ops in pairs:
+            if ops.combine_name == "divide":
+                continue
+            m, k, n = (int(v) for v in rng.integers(1, 9, size=3))
+            lim = 4 if ops.reduce_name == "multiply" else 100
+            a = rng.integers(-lim, lim + 1, size=m * k).astype(dt)
+            b = rng.integers(-lim, lim + 1, size=k * n).astype(dt)
+            add("inner", ops, (m, k), a, (k, n), b, "int_inner", dtype=dt)
+            add("outer", ops, (m,), a[:m], (n,), b[:n], "int_outer", dtype=dt)
+        for ops in (mp.op_pair("multiply", "add"), mp.op_pair("add", "min"),
+                    mp.op_pair("subtract", "max")):
+            m, k, n = 37, 67, 45
+            a = rng.integers(-1000, 1001, size=m * k).astype(dt)
+            b = rng.integers(-1000, 1001, size=k * n).astype(dt)
+            add("inner", ops, (m, k), a, (k, n), b, "int_medium", dtype=dt)
 
     arrays = {}
     for i, (mode, c, r, sa, a, sb, b, out, oshape, tag) in enumerate(cases):

@@ -43,6 +43,8 @@ def test_header_constants_match_python_codes():
         assert int(consts[f"MOA_REDUCE_{name.upper()}"]) == code
     assert int(consts["MOA_DTYPE_F64"]) == _native.DTYPE_F64
     assert int(consts["MOA_DTYPE_F32"]) == _native.DTYPE_F32
+    assert int(consts["MOA_DTYPE_I32"]) == _native.DTYPE_I32
+    assert int(consts["MOA_DTYPE_I64"]) == _native.DTYPE_I64
     assert int(consts["MOA_FLAG_ACCUMULATE"]) == _native.FLAG_ACCUMULATE
     assert int(consts["MOA_FLAG_EXACT"]) == _native.FLAG_EXACT
 
@@ -55,6 +57,9 @@ def test_kernel_routing():
     assert pk(1, 16384, 16384, 16384, 0, 2, _native.FLAG_ACCUMULATE) == "semiring_exact"
     assert pk(0, 16384, 16384, 16384, 0, 2) == "semiring_exact"  # no f64 fast loop
     assert pk(1, 16384, 16384, 16384, 2, 0) == "semiring_exact"  # f32 sums run in f64
+    assert pk(2, 16384, 16384, 16384, 2, 0) == "semiring_exact"  # int32: exact integer fold
+    assert pk(3, 16384, 16384, 16384, 0, 2) == "semiring_exact"  # int64 tropical
+    assert pk(2, 65536, 1, 2048, 2, 0) == "outer"
     assert pk(0, 65536, 1, 2048, 2, 0) == "outer"
     assert pk(0, 2, 0, 3, 2, 2) == "fill"
     assert pk(0, 2, 0, 3, 2, 2, _native.FLAG_ACCUMULATE) == "none"
@@ -72,6 +77,7 @@ def _call(**kw):
 
 @pytest.mark.parametrize("kw, msg", [
     (dict(dtype=7), "dtype"),
+    (dict(dtype=-1), "dtype"),
     (dict(combine_code=6), "combine"),
     (dict(reduce_code=-1), "reduce"),
     (dict(step=0), "step"),

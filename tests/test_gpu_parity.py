@@ -31,7 +31,7 @@ def _torch():
 
 
 def _run(case, exact=False, device=False, workers=1):
-    dt = np.float32 if case.a.dtype == np.float32 else np.float64
+    dt = case.a.dtype
     a = MoaArray(case.shape_a, case.a, dtype=dt)
     b = MoaArray(case.shape_b, case.b, dtype=dt)
     if device:
@@ -52,7 +52,10 @@ def _is_dmma(case) -> bool:
 
 def _check(case, got, exact=False):
     want = case.out
-    if got.dtype == np.float32:
+    if got.dtype.kind == "i":  # integer-valued reference result, exact
+        assert got.dtype == case.a.dtype, repr(case)
+        np.testing.assert_array_equal(got, want.astype(got.dtype), err_msg=repr(case))
+    elif got.dtype == np.float32:
         assert_bits_equal(got, want.astype(np.float32), repr(case))
     elif _is_dmma(case) and not exact:
         k = case.shape_a[-1]
@@ -72,7 +75,9 @@ def test_golden_cases_exact_mode_bitwise_everywhere(golden_small):
     """exact=True reproduces the reference's (multiply, add) rounding too."""
     for case in golden_small:
         got = _run(case, exact=True)
-        if got.dtype == np.float32:
+        if got.dtype.kind == "i":
+            np.testing.assert_array_equal(got, case.out.astype(got.dtype), err_msg=repr(case))
+        elif got.dtype == np.float32:
             assert_bits_equal(got, case.out.astype(np.float32), repr(case))
         else:
             assert_bits_equal(got, case.out, repr(case))
@@ -366,3 +371,39 @@ def test_kernels_never_write_outside_their_rows(rng):
             owned = host[~want_sent]
             assert not np.any(owned == np.array(sentinel, dtype=host.dtype)), \
                 f"owned element left unwritten {(m, k, n)} {ops} {dt}"
+
+
+def test_integer_semantics_beyond_the_reference():
+    """Integer-only behaviour (no float64 reference): wraparound, truncating
+    division with x/0 = 0, and the type's max/min as the min/max identities."""
+    i32 = np.int32
+    big = MoaArray((1, 2), [2**31 - 1, 5], dtype=i32)
+    one = MoaArray((2, 1), [1, 1], dtype=i32)
+    assert moa.inner(big, one).data.tolist() == [np.int32(2**31 - 1 + 5 - 2**32)]
+    num = MoaArray((4,), [7, -7, 5, -2**31], dtype=i32)
+    den = MoaArray((4,), [2, 2, 0, -1], dtype=i32)
+    q = moa.outer(num, den, op_pair("divide", "max")).data.reshape(4, 4)
+    assert q[0].tolist() == [3, 3, 0, -7] and q[1].tolist() == [-3, -3, 0, 7]
+    assert q[3].tolist()[3] == -2**31  # MIN / -1 wraps
+    for dt, info in ((np.int32, np.iinfo(np.int32)), (np.int64, np.iinfo(np.int64))):
+        e = moa.inner(MoaArray((2, 0), [], dtype=dt), MoaArray((0, 3), [], dtype=dt),
+                      op_pair("add", "min"))
+        assert e.data.dtype == dt and e.data.tolist() == [info.max] * 6
+        e = moa.inner(MoaArray((2, 0), [], dtype=dt), MoaArray((0, 3), [], dtype=dt),
+                      op_pair("add", "max"))
+        assert e.data.tolist() == [info.min] * 6
+
+
+def test_integer_large_random_matches_int_reference(rng):
+    """Tile-crossing integer products against numpy's exact int64 matmul."""
+    for dt in (np.int32, np.int64):
+        m, k, n = 300, 129, 257
+        a = rng.integers(-1000, 1000, size=(m, k)).astype(dt)
+        b = rng.integers(-1000, 1000, size=(k, n)).astype(dt)
+        got = moa.inner(MoaArray((m, k), a.ravel(), dtype=dt), MoaArray((k, n), b.ravel(), dtype=dt))
+        assert got.data.dtype == dt
+        np.testing.assert_array_equal(got.data.reshape(m, n), (a.astype(np.int64) @ b).astype(dt))
+        mn = moa.inner(MoaArray((m, k), a.ravel(), dtype=dt), MoaArray((k, n), b.ravel(), dtype=dt),
+                       op_pair("add", "min"))
+        want = (a[:, :, None].astype(np.int64) + b[None, :, :]).min(axis=1).astype(dt)
+        np.testing.assert_array_equal(mn.data.reshape(m, n), want)

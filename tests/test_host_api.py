@@ -65,8 +65,21 @@ def test_moaarray_float32_storage_only_on_request():
     x = np.arange(4, dtype=np.float32)
     assert MoaArray((4,), x).dtype == np.float64  # the reference upcasts
     assert MoaArray((4,), x, dtype=np.float32).dtype == np.float32
+    assert MoaArray((4,), x, dtype=np.int32).dtype == np.int32
     with pytest.raises(TypeError):
-        MoaArray((4,), x, dtype=np.int32)
+        MoaArray((4,), x, dtype=np.int8)
+
+
+def test_result_dtype_promotion():
+    from paper_0907_0792_b200.kernel import result_dtype
+    def arr(dt):
+        return MoaArray((1,), [1], dtype=dt)
+    cases = {(np.float32, np.float32): np.float32, (np.float32, np.float64): np.float64,
+             (np.int32, np.int32): np.int32, (np.int32, np.int64): np.int64,
+             (np.int32, np.float32): np.float64, (np.int64, np.float64): np.float64}
+    for (x, y), want in cases.items():
+        assert result_dtype(arr(x), arr(y)) == np.dtype(want)
+        assert result_dtype(arr(y), arr(x)) == np.dtype(want)
 
 
 def test_psi_select():

@@ -3,7 +3,7 @@
 // shape of semiring_kernel and checks that all give identical bits.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        -o tools/tune_semiring tools/tune_semiring.cu
-#include "../paper_0907_0792_b200/csrc/semiring.cu"
+#include "../paper_0907_0792_b200/csrc/semiring_impl.cuh"
 
 #include <cstdio>
 
