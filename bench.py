@@ -228,7 +228,8 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
     plan = plan_for(w)
     r0, r1 = rows_range
     m, k, n = w.mkn
-    tdt = torch.float32 if w.dtype == np.float32 else torch.float64
+    tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+           np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64}[np.dtype(w.dtype)]
     lda = plan.lstride
     a_dev = torch.from_numpy(np.ascontiguousarray(a_host[r0 * lda:r1 * lda])).to(device)
     b_dev = torch.from_numpy(b_host).to(device) if rank == 0 else \
@@ -238,10 +239,19 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
     flush = L2Flusher(device)
     stream = torch.cuda.current_stream(device)
 
-    def step():
-        if world > 1:
-            dist.broadcast(b_dev, src=0, group=group)
-        launch(sub, c_dev, a_dev, b_dev, w.ops)
+    if world > 1:
+        from paper_0907_0792_b200.distributed import sharded_product
+        gplan = job_plan(w, world)
+        # strong-scaled (x,+) f64 products pipeline B's broadcast in k-chunks
+        chunks = 8 if (SCALING[w.key] == "strong" and w.ops.codes() == (2, 0)
+                       and w.dtype == np.float64) else 1
+
+        def step():
+            sharded_product(gplan, a_dev, b_dev if rank == 0 else None, w.ops, group=group,
+                            out=c_dev, bcast_chunks=chunks)
+    else:
+        def step():
+            launch(sub, c_dev, a_dev, b_dev, w.ops)
 
     for _ in range(warmup):
         step()

@@ -68,14 +68,32 @@ def _cuda_rows(plan: KernelPlan, c, a, b, ops: OpPair, exact: bool = False) -> N
     launch(plan, c, a, b, ops, exact=exact)
 
 
+def k_chunks(K: int, chunks: int, align: int = 16) -> list[tuple[int, int]]:
+    """Split [0, K) into up to ``chunks`` ranges whose inner boundaries are
+    multiples of ``align`` (the DMMA kernel's k-slab), so accumulating the
+    chunks replays exactly the DMMA sequence of one pass."""
+    if chunks <= 1 or K <= align:
+        return [(0, K)]
+    step = -(-K // chunks)
+    step = -(-step // align) * align
+    return [(k0, min(K, k0 + step)) for k0 in range(0, K, step)]
+
+
 def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, group=None,
                     src: int = 0, exact: bool = False, out=None,
-                    row_kernel: Callable | None = None):
+                    row_kernel: Callable | None = None, bcast_chunks: int = 1):
     """This rank's result block of ``plan``.
 
     a_block: this rank's rows of A (flat, rows row_block(...)), on this rank's
     device; b: the full B on rank ``src`` (ignored elsewhere).  Returns the flat
     result block (rows r0..r1 of C) on the same device as a_block.
+
+    ``bcast_chunks > 1`` pipelines the broadcast of B with the compute for
+    (multiply, add) on float64: B is broadcast in k-chunks (asynchronously, in
+    order) and the kernel for chunk i runs as soon as chunk i has arrived,
+    accumulating into C (MOA_FLAG_ACCUMULATE) while later chunks are still on
+    the wire.  Chunk boundaries are multiples of the DMMA k-slab, so the
+    result is bitwise identical to one pass.
     """
     torch, dist = _torch(), _dist()
     world, rank = dist.get_world_size(group), dist.get_rank(group)
@@ -84,13 +102,32 @@ def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, grou
     if a_block.numel() != (r1 - r0) * plan.lstride:
         raise ValueError(f"rank {rank} owns rows [{r0}, {r1}) = {(r1 - r0) * plan.lstride} "
                          f"A elements, got {a_block.numel()}")
-    b_all = broadcast_operand(b, plan, src=src, group=group, device=a_block.device,
-                              dtype=a_block.dtype)
     c = out if out is not None else torch.empty(sub.noproc * sub.elsinop,
                                                 dtype=a_block.dtype, device=a_block.device)
-    if sub.noproc:
-        (row_kernel or (lambda p, c_, a_, b_, o: _cuda_rows(p, c_, a_, b_, o, exact)))(
-            sub, c, a_block, b_all, ops)
+    pipelined = (bcast_chunks > 1 and row_kernel is None and not exact
+                 and ops.codes() == (2, 0) and a_block.dtype == torch.float64)
+    if not pipelined:
+        b_all = broadcast_operand(b, plan, src=src, group=group, device=a_block.device,
+                                  dtype=a_block.dtype)
+        if sub.noproc:
+            (row_kernel or (lambda p, c_, a_, b_, o: _cuda_rows(p, c_, a_, b_, o, exact)))(
+                sub, c, a_block, b_all, ops)
+        return c
+    # pipelined: async, in-order broadcasts of B's k-chunks; compute chases them
+    n, k = plan.elsinop, plan.rowsinred
+    if rank == src:
+        b_all = b.reshape(-1).to(a_block.device).contiguous()
+    else:
+        b_all = torch.empty(k * n, dtype=a_block.dtype, device=a_block.device)
+    chunks = k_chunks(k, bcast_chunks)
+    works = [dist.broadcast(b_all[k0 * n:k1 * n], src=src, group=group, async_op=True)
+             for k0, k1 in chunks]
+    for i, ((k0, k1), work) in enumerate(zip(chunks, works)):
+        work.wait()  # the current stream waits for this chunk only
+        if sub.noproc:
+            part = KernelPlan(plan.mode, sub.noproc, k1 - k0, n, plan.lstride, plan.rstride,
+                              plan.restride, plan.result_shape)
+            launch(part, c, a_block[k0:], b_all[k0 * n:], ops, accumulate=i > 0)
     return c
 
 

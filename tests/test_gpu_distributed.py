@@ -44,6 +44,18 @@ def _worker(rank, world, port, q):
             if rank == 0:
                 ref = moa.inner(moa.MoaArray((m, k), a), moa.MoaArray((k, n), b), ops).data
                 ok &= bool(torch.equal(full.view(-1), ref.view(-1)))
+        # pipelined broadcast of B in k-chunks (float64 (x,+)): same bits
+        m, k, n = 500, 300, 384
+        a = torch.from_numpy(rng.random(m * k)).cuda()
+        b = torch.from_numpy(rng.random(k * n)).cuda()
+        plan = moa.plan_inner((m, k), (k, n))
+        r0, r1 = row_block(m, world, rank)
+        blk = sharded_product(plan, a[r0 * k:r1 * k], b if rank == 0 else None, moa.MUL_ADD,
+                              bcast_chunks=4)
+        full = gather_rows(blk, plan)
+        if rank == 0:
+            ref = moa.inner(moa.MoaArray((m, k), a), moa.MoaArray((k, n), b)).data
+            ok &= bool(torch.equal(full.view(-1), ref.view(-1)))
         # the host-buffer form used by bench.py's e2e leg
         from paper_0907_0792_b200.distributed import sharded_product_host
         m, k, n = 100, 64, 96

@@ -407,3 +407,20 @@ def test_integer_large_random_matches_int_reference(rng):
                        op_pair("add", "min"))
         want = (a[:, :, None].astype(np.int64) + b[None, :, :]).min(axis=1).astype(dt)
         np.testing.assert_array_equal(mn.data.reshape(m, n), want)
+
+
+def test_k_chunked_accumulation_replays_one_pass(rng):
+    """Accumulating k-chunks (slab-aligned) with MOA_FLAG_ACCUMULATE gives the
+    bits of one DMMA pass — what the pipelined broadcast of B relies on."""
+    torch = _torch()
+    from paper_0907_0792_b200.distributed import k_chunks
+    m, k, n = 700, 1000, 520
+    a, b = _dev(rng.random(m * k) * 2 - 1), _dev(rng.random(k * n) * 2 - 1)
+    one = torch.empty(m * n, dtype=torch.float64, device="cuda")
+    launch(plan_inner((m, k), (k, n)), one, a, b, moa.MUL_ADD)
+    for chunks in (2, 3, 8):
+        c = torch.empty(m * n, dtype=torch.float64, device="cuda")
+        for i, (k0, k1) in enumerate(k_chunks(k, chunks)):
+            part = moa.KernelPlan(moa.ProductMode.INNER, m, k1 - k0, n, k, n, n, (m, n))
+            launch(part, c, a[k0:], b[k0 * n:], moa.MUL_ADD, accumulate=i > 0)
+        assert torch.equal(c, one), chunks
