@@ -257,6 +257,7 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
         step()
     torch.cuda.synchronize(device)
     if world > 1:
+        dist.broadcast(b_dev, src=0, group=group)  # the kernel-only leg below reads b_dev
         dist.barrier()
     torch.cuda.synchronize(device)
     launches0 = _native.launch_count()
