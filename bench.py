@@ -162,12 +162,6 @@ def dist_env() -> tuple[int, int, int]:
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def rank_inputs(w, rank: int):
-    """The unit of work this rank owns (A rows; B as drawn by rank 0)."""
-    a, b = w.generate()
-    return a, b
-
-
 def pinned_copy(x: np.ndarray):
     import torch
     t = torch.empty(x.size, dtype=torch.from_numpy(x[:1]).dtype, pin_memory=True)

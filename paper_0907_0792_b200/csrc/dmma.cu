@@ -252,10 +252,12 @@ cudaError_t dmma_launch(const Problem& p) {
 }
 
 // Tile configurations (tools/tune_dmma.cu sweep, profiles/r01_tune_dmma*.jsonl):
-// large: 64x128 CTA, 8 warps of 32x32, 4 stages, 2 CTAs/SM  -> 88.9% of peak at c4
+// large: 64x128 CTA, 8 warps of 32x32, 4 stages, 2 CTAs/SM  -> 88.9% of peak at c4;
+//        groups of 16 row tiles (tools/traffic_dmma.cu: 83 GB of DRAM reads per c4
+//        launch vs 94 GB for 8, same time)
 // medium: 64x64 CTA, 4 warps of 32x32, 3 stages, 3 CTAs/SM
 // small: 32x32 CTA, 4 warps of 16x16, BK=32 (few k-tile round trips; c1-sized problems)
-using CfgLarge = DmmaCfg<64, 128, 32, 32, 4, 16, 2>;
+using CfgLarge = DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>;
 using CfgMedium = DmmaCfg<64, 64, 32, 32, 3, 16, 3>;
 using CfgSmall = DmmaCfg<32, 32, 16, 16, 3, 32, 1>;
 
