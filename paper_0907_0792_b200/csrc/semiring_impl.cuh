@@ -355,6 +355,14 @@ cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
   return cudaGetLastError();
 }
 
+}  // namespace
+}  // namespace moa
+
+#include "tropical.cuh"
+
+namespace moa {
+namespace {
+
 template <typename T, int C, int R>
 cudaError_t semiring_acc(const Problem& p) {
   if (p.accumulate) return semiring_launch<T, C, R, true, -1>(p, nullptr);
@@ -370,8 +378,8 @@ cudaError_t semiring_acc(const Problem& p) {
     launch_scan<T>(static_cast<const T*>(p.a), p.M, p.K, p.lda, special, p.stream);
     launch_scan<T>(static_cast<const T*>(p.b), p.K, p.N, p.ldb, special + 1, p.stream);
     // one specialisation per fold mode; all but the selected one exit at once
-    if constexpr (C == C_ADD) e = semiring_launch<T, C, R, false, 2>(p, special);
-    if (e == cudaSuccess) e = semiring_launch<T, C, R, false, 1>(p, special);
+    if constexpr (C == C_ADD) e = tropical_launch<C, R, 2>(p, special);
+    if (e == cudaSuccess) e = tropical_launch<C, R, 1>(p, special);
     if (e == cudaSuccess) e = semiring_launch<T, C, R, false, 0>(p, special);
     cudaError_t e2 = cudaFreeAsync(special, p.stream);
     return e != cudaSuccess ? e : e2;

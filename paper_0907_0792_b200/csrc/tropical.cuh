@@ -1,0 +1,232 @@
+// K2 fast loops for the float32 tropical semirings — combine in {add, subtract},
+// reduce in {min, max} (BASELINE config 5) — in their own kernel.
+//
+// Operands stay in their natural row-major layouts in shared memory
+// (A[BM][BK+4], B[BK][BN+4]) so both tiles are filled with 16-byte cp.async
+// chunks.  A thread owns rows ty*8+i and columns 64g + 4tx + c (g < 2, c < 4)
+// of a 128x128 C tile.  For each k-pair (k, k+1) it forms, per row i and
+// column pair (j, j+1),
+//     s  = FADD2((B[k][j],   B[k][j+1]),   a[i][k]   broadcast)
+//     s' = FADD2((B[k+1][j], B[k+1][j+1]), a[i][k+1] broadcast)
+//     acc[i][j]   = min3(acc[i][j],   s.x, s'.x)
+//     acc[i][j+1] = min3(acc[i][j+1], s.y, s'.y)
+// i.e. one packed add and one 3-input fold per two (a, b) pairs, with the B
+// operand straight from a 64-bit shared load.  The fold is VIMNMX3 on the bit
+// patterns (mode 2: every combine result is a non-negative float) or FMNMX3
+// (mode 1: no combine result can be NaN or -0.0); see tropical_fold_mode.
+// Both are exact (bit-identical to the reference's compare-select fold) under
+// their conditions, which the device pre-scan establishes; the kernel returns
+// at once when the pre-scan selected another mode.
+#pragma once
+
+#include "moa_common.cuh"
+
+namespace moa {
+namespace {
+
+constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3, TNT = 256;
+constexpr int TLDA = TBK + 4, TLDB = TBN + 4;  // floats; rows stay 16-byte aligned
+constexpr int TA_STAGE = TBM * TLDA, TB_STAGE = TBK * TLDB;
+constexpr size_t TSMEM = (size_t)TSTAGES * (TA_STAGE + TB_STAGE) * sizeof(float);
+
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(bytes)
+               : "memory");
+}
+
+// (x0 op a, x1 op a) with the scalar a broadcast to both lanes
+template <int C>
+__device__ __forceinline__ unsigned long long pair_op_bcast(float x0, float x1, float a) {
+  unsigned long long r;
+  if (C == C_SUB)  // combine(a, b) = a - b, A element first (_ckernel.pyx:71)
+    asm("{\n\t.reg .b64 ta, tb;\n\tmov.b64 ta, {%1, %1};\n\tmov.b64 tb, {%2, %3};\n\t"
+        "sub.rn.f32x2 %0, ta, tb;\n\t}"
+        : "=l"(r) : "f"(a), "f"(x0), "f"(x1));
+  else
+    asm("{\n\t.reg .b64 ta, tb;\n\tmov.b64 ta, {%1, %1};\n\tmov.b64 tb, {%2, %3};\n\t"
+        "add.rn.f32x2 %0, tb, ta;\n\t}"
+        : "=l"(r) : "f"(a), "f"(x0), "f"(x1));
+  return r;
+}
+__device__ __forceinline__ float lo32(unsigned long long v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi32(unsigned long long v) {
+  return __uint_as_float((unsigned)(v >> 32));
+}
+
+template <int C, int R, int MODE, bool VEC>
+__global__ void __launch_bounds__(TNT, 2)
+    tropical_kernel(float* __restrict__ c, const float* __restrict__ a, const float* __restrict__ b,
+                    int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                    const unsigned* special, int64_t tiles_m, int64_t tiles_n) {
+  static_assert(MODE == 1 || MODE == 2, "fast modes only");
+  constexpr bool INTFOLD = MODE == 2;
+  if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODE) return;
+  extern __shared__ __align__(16) float tsm[];
+  float* As = tsm;
+  float* Bs = tsm + TSTAGES * TA_STAGE;
+
+  const int64_t pid = blockIdx.x;
+  constexpr int GM = 8;
+  const int64_t width = GM * tiles_n;
+  const int64_t first_m = (pid / width) * GM;
+  const int64_t gsize = (tiles_m - first_m) < GM ? (tiles_m - first_m) : GM;
+  const int64_t m0 = (first_m + (pid % width) % gsize) * TBM;
+  const int64_t n0 = ((pid % width) / gsize) * TBN;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+
+  float acc[8][8];
+  const float init = (INTFOLD && R == R_MAX) ? 0.0f  // see semiring_kernel: mode 2 max folds from +0
+                                            : ReduceOp<R>::template identity<float>();
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc[i][j] = init;
+
+  // ---- loaders: 16-byte chunks (VEC) or single elements, zero-filled outside ----
+  auto load_stage = [&](int stage, int64_t k0) {
+    float* as = As + stage * TA_STAGE;
+    float* bs = Bs + stage * TB_STAGE;
+    if constexpr (VEC) {
+#pragma unroll
+      for (int q = 0; q < TBM * TBK / 4 / TNT; q++) {  // 4 chunks per thread
+        const int ch = tid + q * TNT, r = ch >> 3, kc = (ch & 7) * 4;
+        const int64_t gm = m0 + r, gk = k0 + kc;
+        int64_t rem = gm < M ? K - gk : 0;
+        rem = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+        cp_async16_zfill(as + r * TLDA + kc, rem ? a + gm * lda + gk : a, (int)rem * 4);
+      }
+#pragma unroll
+      for (int q = 0; q < TBK * TBN / 4 / TNT; q++) {  // 4 chunks per thread
+        const int ch = tid + q * TNT, r = ch >> 5, nc = (ch & 31) * 4;
+        const int64_t gk = k0 + r, gn = n0 + nc;
+        int64_t rem = gk < K ? N - gn : 0;
+        rem = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+        cp_async16_zfill(bs + r * TLDB + nc, rem ? b + gk * ldb + gn : b, (int)rem * 4);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < TBM * TBK / TNT; q++) {
+        const int e = tid + q * TNT, r = e / TBK, kk = e % TBK;
+        const int64_t gm = m0 + r, gk = k0 + kk;
+        const bool ok = gm < M && gk < K;
+        cp_async_elem<4>(as + r * TLDA + kk, ok ? a + gm * lda + gk : a, ok);
+      }
+#pragma unroll
+      for (int q = 0; q < TBK * TBN / TNT; q++) {
+        const int e = tid + q * TNT, r = e / TBN, nn = e % TBN;
+        const int64_t gk = k0 + r, gn = n0 + nn;
+        const bool ok = gk < K && gn < N;
+        cp_async_elem<4>(bs + r * TLDB + nn, ok ? b + gk * ldb + gn : b, ok);
+      }
+    }
+  };
+
+  const int64_t KT = (K + TBK - 1) / TBK;
+#pragma unroll
+  for (int s = 0; s < TSTAGES - 1; s++) {
+    if (s < KT) load_stage(s, (int64_t)s * TBK);
+    cp_async_commit();
+  }
+
+  for (int64_t kt = 0; kt < KT; kt++) {
+    cp_async_wait<TSTAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t nk = kt + TSTAGES - 1;
+      if (nk < KT) load_stage((int)(nk % TSTAGES), nk * TBK);
+      cp_async_commit();
+    }
+    const float* as = As + (int)(kt % TSTAGES) * TA_STAGE + (ty * 8) * TLDA;
+    const float* bs = Bs + (int)(kt % TSTAGES) * TB_STAGE + 4 * tx;
+    const int64_t krem = K - kt * TBK;
+    const int kend = krem < TBK ? (int)krem : TBK;
+
+    // one k-pair (k, k+1): B rows k and k+1 as 16-byte loads, A pair per row as
+    // one 8-byte (broadcast) load
+    auto kpair = [&](int k) {
+      float4 b0[2], b1[2];
+#pragma unroll
+      for (int g = 0; g < 2; g++) {
+        b0[g] = *reinterpret_cast<const float4*>(bs + k * TLDB + 64 * g);
+        b1[g] = *reinterpret_cast<const float4*>(bs + (k + 1) * TLDB + 64 * g);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const float2 av = *reinterpret_cast<const float2*>(as + i * TLDA + k);
+#pragma unroll
+        for (int g = 0; g < 2; g++) {
+#pragma unroll
+          for (int p = 0; p < 2; p++) {
+            const float x0 = p ? b0[g].z : b0[g].x, x1 = p ? b0[g].w : b0[g].y;
+            const float y0 = p ? b1[g].z : b1[g].x, y1 = p ? b1[g].w : b1[g].y;
+            const unsigned long long s = pair_op_bcast<C>(x0, x1, av.x);
+            const unsigned long long t = pair_op_bcast<C>(y0, y1, av.y);
+            const int j = 4 * g + 2 * p;
+            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], lo32(s), lo32(t));
+            acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], hi32(s), hi32(t));
+          }
+        }
+      }
+    };
+    const int npairs = kend >> 1;
+#pragma unroll 1
+    for (int kp = 0; kp < npairs; kp++) kpair(2 * kp);
+    {
+      const int k4 = 2 * npairs;
+      if (k4 < kend) {  // lone last k: scalar combine + 2-input fold
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const float av = as[i * TLDA + k4];
+#pragma unroll
+          for (int g = 0; g < 2; g++)
+#pragma unroll
+            for (int cc = 0; cc < 4; cc++)
+              acc[i][4 * g + cc] =
+                  ReduceOp<R>::f(acc[i][4 * g + cc], CombineOp<C>::f(av, bs[k4 * TLDB + 64 * g + cc]));
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  const bool vec_store = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(c) % 16 == 0);
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int64_t row = m0 + ty * 8 + i;
+    if (row >= M) continue;
+#pragma unroll
+    for (int g = 0; g < 2; g++) {
+      const int64_t col = n0 + 64 * g + 4 * tx;
+      if (vec_store && col + 3 < N) {
+        *reinterpret_cast<float4*>(c + row * ldc + col) =
+            make_float4(acc[i][4 * g], acc[i][4 * g + 1], acc[i][4 * g + 2], acc[i][4 * g + 3]);
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < 4; cc++)
+          if (col + cc < N) c[row * ldc + col + cc] = acc[i][4 * g + cc];
+      }
+    }
+  }
+}
+
+template <int C, int R, int MODE>
+cudaError_t tropical_launch(const Problem& p, const unsigned* special) {
+  const bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) &&
+                   (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
+  auto kern = vec ? tropical_kernel<C, R, MODE, true> : tropical_kernel<C, R, MODE, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
+  const int64_t tiles = tiles_m * tiles_n;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)tiles, TNT, TSMEM, p.stream>>>(
+      static_cast<float*>(p.c), static_cast<const float*>(p.a), static_cast<const float*>(p.b),
+      p.M, p.N, p.K, p.lda, p.ldb, p.ldc, special, tiles_m, tiles_n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace moa
