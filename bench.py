@@ -375,7 +375,7 @@ def measure_e2e(w, rows_range, a_pin, b_pin, steps, warmup, device, world, rank,
 
 
 # ---------------------------------------------------------------------------- CPU legs
-def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 20, rows: int | None = None):
+def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 500, rows: int | None = None):
     """Reference hot loop (oracle/_ref, else the C port) on all host cores.
 
     Returns (seconds per unit of ``rows`` rows, kind, cores, sample description)."""
@@ -391,7 +391,7 @@ def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 20, rows
         (lambda: oracle.product(a_s, b, rows, k, n, comb, red, workers=cores))
     times = []
     t_end = time.perf_counter() + budget_s
-    while len(times) < max_reps and (not times or time.perf_counter() < t_end):
+    while len(times) < max_reps and (len(times) < 3 or time.perf_counter() < t_end):
         t0 = time.perf_counter()
         run()
         times.append(time.perf_counter() - t0)
