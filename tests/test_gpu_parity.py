@@ -424,3 +424,38 @@ def test_k_chunked_accumulation_replays_one_pass(rng):
             part = moa.KernelPlan(moa.ProductMode.INNER, m, k1 - k0, n, k, n, n, (m, n))
             launch(part, c, a[k0:], b[k0 * n:], moa.MUL_ADD, accumulate=i > 0)
         assert torch.equal(c, one), chunks
+
+
+def test_concurrent_invocations_are_reentrant(rng):
+    """reference tests/test_parallel.py:86-96: the executor is reentrant
+    across host threads sharing operands (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    m, k, n = 300, 200, 260
+    a = MoaArray((m, k), rng.random(m * k))
+    b = MoaArray((k, n), rng.random(k * n))
+    plan = moa.plan_inner(a.shape, b.shape)
+    for ops in (moa.MUL_ADD, op_pair("add", "min")):
+        want = moa.execute_sequential(plan, a, b, ops).data
+        with ThreadPoolExecutor(max_workers=6) as pool:
+            futs = [pool.submit(moa.execute_parallel, plan, a, b, ops, 1 + i % 4)
+                    for i in range(12)]
+            for f in futs:
+                assert_bits_equal(f.result().data, want)
+
+
+def test_workers_over_repeated_devices_bitwise(rng):
+    """execute_parallel's multi-block path (several blocks on the one GPU)
+    reproduces the single launch bit for bit, host and device operands."""
+    m, k, n = 517, 130, 333
+    a = MoaArray((m, k), rng.random(m * k))
+    b = MoaArray((k, n), rng.random(k * n))
+    plan = moa.plan_inner(a.shape, b.shape)
+    for ops in (moa.MUL_ADD, op_pair("subtract", "max")):
+        want = moa.execute_sequential(plan, a, b, ops).data
+        for devs in ([0, 0], [0, 0, 0, 0, 0]):
+            got = moa.execute_parallel(plan, a, b, ops, workers=len(devs), devices=devs)
+            assert_bits_equal(got.data, want)
+            got = moa.execute_parallel(plan, a.to_device(), b.to_device(), ops,
+                                       workers=len(devs), devices=devs)
+            assert got.is_device
+            assert_bits_equal(got.host_data(), want)
