@@ -254,6 +254,20 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
         dist.broadcast(b_dev, src=0, group=group)  # the kernel-only leg below reads b_dev
         dist.barrier()
     torch.cuda.synchronize(device)
+    # Single GPU: the step is captured once into a CUDA graph, so each timed
+    # step is one graph launch and the events bracket device work only (no
+    # host-side launch gaps).  N>1 keeps eager steps (the broadcast inside may
+    # run over gloo, which cannot be captured).
+    graph, per_step_launches = None, None
+    if world == 1:
+        l0 = _native.launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        per_step_launches = _native.launch_count() - l0
+        graph.replay()
+        torch.cuda.synchronize(device)
+    run_step = graph.replay if graph is not None else step
     launches0 = _native.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
@@ -261,10 +275,11 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
         for s, e in evs:
             flush()
             s.record(stream)
-            step()
+            run_step()
             e.record(stream)
         torch.cuda.synchronize(device)
-        launches = _native.launch_count() - launches0
+        launches = (per_step_launches * steps if graph is not None
+                    else _native.launch_count() - launches0)
         step_ms = sum(s.elapsed_time(e) for s, e in evs)
         # Short timed regions end before nvidia-smi samples them: keep the same
         # load running (untimed, same count on every rank) until the sampler
@@ -278,7 +293,7 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
         for i in range(extra):
             if i % 8 == 0:
                 flush()
-            step()
+            run_step()
         torch.cuda.synchronize(device)
     if world > 1:
         dist.barrier()
@@ -290,13 +305,17 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
     for s, e in kev:
         flush()
         s.record(stream)
-        launch(sub, c_dev, a_dev, b_dev, w.ops)
+        if graph is not None:
+            graph.replay()  # at N=1 the step is exactly the product launch
+        else:
+            launch(sub, c_dev, a_dev, b_dev, w.ops)
         e.record(stream)
     torch.cuda.synchronize(device)
     kern_ms = [s.elapsed_time(e) for s, e in kev]
     del a_dev, b_dev, c_dev, flush
     return {"step_ms_total": step_ms, "kernel_ms_mean": sum(kern_ms) / len(kern_ms),
-            "kernel_ms_min": min(kern_ms), "launches": launches, "clocks": clocks.summary()}
+            "kernel_ms_min": min(kern_ms), "launches": launches, "clocks": clocks.summary(),
+            "graph": graph is not None}
 
 
 def roofline(w, rows: int, kernel_ms: float) -> dict:
@@ -533,7 +552,8 @@ def main() -> None:
                        "rows_per_rank": rows_range[1] - rows_range[0],
                        "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1
                        else "single GPU",
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "cuda_graph": bool(dev.get("graph"))},
             "e2e": {"value": round(e2e_value, 3), "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "moa.outer/inner on pinned host MoaArrays" if world == 1 else
