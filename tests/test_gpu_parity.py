@@ -459,3 +459,20 @@ def test_workers_over_repeated_devices_bitwise(rng):
                                        workers=len(devs), devices=devs)
             assert got.is_device
             assert_bits_equal(got.host_data(), want)
+
+
+def test_oracle_api_mirrors_reference_definitions(golden_small):
+    """oracle_inner / oracle_outer (reference oracle.py:33-72) exported for API
+    parity: inner = the exact fold, outer = combine with no reduce."""
+    for case in golden_small[::9]:
+        if case.a.dtype != np.float64:
+            continue
+        ops = op_pair(list(moa.COMBINE_OPS)[case.comb], list(moa.REDUCE_OPS)[case.red])
+        a, b = MoaArray(case.shape_a, case.a), MoaArray(case.shape_b, case.b)
+        if case.mode == "inner":
+            assert_bits_equal(moa.oracle_inner(a, b, ops).data, case.out, repr(case))
+        else:
+            want = oracle.odometer_outer(case.a, case.shape_a, case.b, case.shape_b, case.comb)
+            assert_bits_equal(moa.oracle_outer(a, b, ops).data, want, repr(case))
+    neg = moa.oracle_outer(MoaArray((), [-1.0]), MoaArray((), [0.0]))
+    assert np.signbit(neg.item())  # combine only: (-1)*0 = -0.0, no "+ 0.0"
