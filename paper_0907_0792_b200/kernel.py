@@ -191,6 +191,7 @@ def launch(plan: KernelPlan, res, a_dev, b_dev, ops: OpPair, *, start: int = 0,
     codes = ops.codes()
     if codes is None:
         raise ValueError("custom OpPair callables have no device implementation")
+    _check_extents(plan, res, a_dev, b_dev, start, step)
     if stream is None:
         stream = torch.cuda.current_stream(res.device)
     flags = (_native.FLAG_EXACT if exact else 0) | (_native.FLAG_ACCUMULATE if accumulate else 0)
@@ -198,6 +199,27 @@ def launch(plan: KernelPlan, res, a_dev, b_dev, ops: OpPair, *, start: int = 0,
                          plan.noproc, plan.rowsinred, plan.elsinop,
                          plan.lstride, plan.rstride, plan.restride,
                          codes[0], codes[1], start, step, flags, stream.cuda_stream)
+
+
+def _check_extents(plan: KernelPlan, res, a_dev, b_dev, start: int, step: int) -> None:
+    """The kernels index raw pointers: refuse tensors that are not flat,
+    contiguous, on one CUDA device, and long enough for the rows addressed."""
+    for name, t in (("res", res), ("a", a_dev), ("b", b_dev)):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous CUDA tensor")
+    if not (res.device == a_dev.device == b_dev.device):
+        raise ValueError("res, a and b must be on one device")
+    if step < 1 or start < 0 or start >= plan.noproc or plan.elsinop == 0:
+        return  # nothing is touched (the C ABI rejects step < 1 / start < 0)
+    last = start + (plan.noproc - 1 - start) // step * step
+    need = {"res": last * plan.restride + plan.elsinop}
+    if plan.rowsinred:
+        need["a"] = last * plan.lstride + plan.rowsinred
+        need["b"] = (plan.rowsinred - 1) * plan.rstride + plan.elsinop
+    have = {"res": res.numel(), "a": a_dev.numel(), "b": b_dev.numel()}
+    for name, n in need.items():
+        if have[name] < n:
+            raise ValueError(f"{name} holds {have[name]} elements; the plan addresses {n}")
 
 
 class _Runner:

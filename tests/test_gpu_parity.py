@@ -476,3 +476,23 @@ def test_oracle_api_mirrors_reference_definitions(golden_small):
             assert_bits_equal(moa.oracle_outer(a, b, ops).data, want, repr(case))
     neg = moa.oracle_outer(MoaArray((), [-1.0]), MoaArray((), [0.0]))
     assert np.signbit(neg.item())  # combine only: (-1)*0 = -0.0, no "+ 0.0"
+
+
+def test_launch_refuses_short_or_foreign_buffers():
+    torch = _torch()
+    plan = plan_inner((10, 4), (4, 6))
+    a = torch.zeros(40, dtype=torch.float64, device="cuda")
+    b = torch.zeros(24, dtype=torch.float64, device="cuda")
+    c = torch.zeros(60, dtype=torch.float64, device="cuda")
+    launch(plan, c, a, b, moa.MUL_ADD)
+    with pytest.raises(ValueError, match="res holds"):
+        launch(plan, c[:59], a, b, moa.MUL_ADD)
+    with pytest.raises(ValueError, match="a holds"):
+        launch(plan, c, a[:39], b, moa.MUL_ADD)
+    with pytest.raises(ValueError, match="b holds"):
+        launch(plan, c, a, b[:23], moa.MUL_ADD)
+    with pytest.raises(ValueError, match="contiguous CUDA"):
+        launch(plan, c, a.cpu(), b, moa.MUL_ADD)
+    with pytest.raises(ValueError, match="contiguous CUDA"):
+        launch(plan, c.view(6, 10).t(), a, b, moa.MUL_ADD)
+    launch(plan, c[:54], a, b, moa.MUL_ADD, start=0, step=4)  # rows 0, 4, 8 -> needs 8*6+6 = 54
