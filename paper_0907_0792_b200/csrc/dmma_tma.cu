@@ -1,0 +1,291 @@
+// K1 with TMA staging: the (multiply, add) float64 kernel of dmma.cu with its
+// operand tiles brought in by the Tensor Memory Accelerator
+// (cp.async.bulk.tensor, SASS UTMALDG) instead of per-thread cp.async.
+//
+// One elected thread issues, per 16-deep k-slab, one 2-D TMA box of A
+// (64 rows x 16 doubles) and eight boxes of B (16 rows x 16 doubles), all
+// completing on one mbarrier per pipeline stage; the other threads only wait
+// on that barrier and run DMMA.  TMA zero-fills everything outside M x K and
+// K x N, so edges need no code at all.
+//
+// Boxes land with the 128-byte swizzle (16-byte chunk c of 128-byte line r
+// stored at chunk c ^ (r & 7)).  The m16n8k4 fragment pattern would still hit
+// the same banks four times per half-warp, so the MMA rows and columns are
+// relabelled instead of the data: MMA row g of a 16-row block reads tile row
+// sigma(g) = 2(g&3) + ((g>>2)&1) + 8(g>>3), and MMA column g of the n8 block
+// pair (2q, 2q+1) reads tile column 16q + pi(g) with pi = {0,1,8,9,2,3,10,11}
+// / {4,5,12,13,6,7,14,15}.  Every fragment LDS.64 is then conflict-free, and
+// the epilogue writes each accumulator pair to the relabelled (still
+// contiguous) positions.  Each C element still accumulates k in ascending
+// 4-wide DMMA steps from k = 0, so the bits equal every dmma.cu configuration.
+#include <cuda.h>
+
+#include "moa_common.cuh"
+#include "moa_kernels.h"
+#include "../../include/moa_b200.h"
+
+namespace moa {
+
+namespace {
+
+constexpr int TM_BM = 64, TM_BN = 128, TM_BK = 16, TM_WM = 32, TM_WN = 32, TM_STAGES = 4;
+constexpr int TM_THREADS = 32 * (TM_BM / TM_WM) * (TM_BN / TM_WN);  // 256
+constexpr int TM_MI = TM_WM / 16, TM_NI = TM_WN / 8;
+constexpr int TM_A_BYTES = TM_BM * TM_BK * 8;           // 8 KiB
+constexpr int TM_B_BYTES = TM_BK * TM_BN * 8;           // 16 KiB (8 boxes of 2 KiB)
+constexpr int TM_STAGE_BYTES = TM_A_BYTES + TM_B_BYTES;
+constexpr size_t TM_SMEM = (size_t)TM_STAGES * TM_STAGE_BYTES + 1024 /*align*/ + 128 /*barriers*/;
+constexpr int TM_WARPS = TM_THREADS / 32;
+constexpr int TM_GROUP_M = 16;
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma_step(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0, %1, %2, %3}, {%4, %5}, {%6}, "
+      "{%0, %1, %2, %3};"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// tile row of MMA row g (0..15) inside a 16-row block; tile column offset of
+// MMA column g (0..7) for the even (h=0) / odd (h=1) n8 block of a pair
+__device__ __forceinline__ int sigma(int g) { return 2 * (g & 3) + ((g >> 2) & 1) + 8 * (g >> 3); }
+__device__ __forceinline__ int pi_col(int g, int h) {
+  return ((g >> 1) & 1) * 8 + (g & 1) + 2 * (g >> 2) + 4 * h;
+}
+// byte offset of element (r, k) in a swizzled A stage (64 lines of 128 B)
+__device__ __forceinline__ int a_off(int r, int k) {
+  return r * 128 + ((((k >> 1) ^ r) & 7) << 4) + ((k & 1) << 3);
+}
+// byte offset of element (k, n) in a swizzled B stage (8 boxes of 16 lines x 128 B)
+__device__ __forceinline__ int b_off(int k, int n) {
+  return (n >> 4) * 2048 + k * 128 + (((((n & 15) >> 1) ^ k) & 7) << 4) + ((n & 1) << 3);
+}
+
+template <bool ACC>
+__global__ void __launch_bounds__(TM_THREADS, 2)
+    dmma_tma_kernel(double* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
+                    int64_t tiles_m, int64_t tiles_n, const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b) {
+  extern __shared__ __align__(16) unsigned char tm_raw[];
+  // swizzle-128B destinations must be 1024-byte aligned
+  // (offset from tm_raw rather than integer rounding of the pointer, so the
+  // compiler keeps the shared address space: LDS, not generic LD)
+  unsigned char* base = tm_raw + ((1024u - (smem_addr(tm_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + TM_STAGES * TM_STAGE_BYTES);
+  uint64_t* empty = full + TM_STAGES;  // one arrival per warp when it is done with a slab
+
+  const int64_t pid = blockIdx.x;
+  const int64_t width = TM_GROUP_M * tiles_n;
+  const int64_t first_m = (pid / width) * TM_GROUP_M;
+  const int64_t gsize = (tiles_m - first_m) < TM_GROUP_M ? (tiles_m - first_m) : TM_GROUP_M;
+  const int64_t m0 = (first_m + (pid % width) % gsize) * TM_BM;
+  const int64_t n0 = ((pid % width) / gsize) * TM_BN;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp / (TM_BN / TM_WN)) * TM_WM, wn0 = (warp % (TM_BN / TM_WN)) * TM_WN;
+  const int g = lane >> 2, t = lane & 3;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < TM_STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TM_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t KT = (K + TM_BK - 1) / TM_BK;
+  auto issue = [&](int stage, int64_t kt) {  // one thread
+    unsigned char* st = base + stage * TM_STAGE_BYTES;
+    mbar_expect_tx(&full[stage], TM_STAGE_BYTES);
+    tma_load_2d(st, &map_a, (int)(kt * TM_BK), (int)m0, &full[stage]);
+#pragma unroll
+    for (int j = 0; j < TM_BN / 16; j++)
+      tma_load_2d(st + TM_A_BYTES + j * 2048, &map_b, (int)(n0 + 16 * j), (int)(kt * TM_BK),
+                  &full[stage]);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < TM_STAGES; s++)
+      if (s < KT) issue(s, s);
+  }
+
+  // per-thread fragment offsets (bytes within a stage), fixed for the kernel
+  int a_row[TM_MI][2];
+#pragma unroll
+  for (int mi = 0; mi < TM_MI; mi++) {
+    a_row[mi][0] = wm0 + mi * 16 + sigma(g);
+    a_row[mi][1] = wm0 + mi * 16 + sigma(g + 8);
+  }
+  int b_col[TM_NI];
+#pragma unroll
+  for (int ni = 0; ni < TM_NI; ni++) b_col[ni] = wn0 + 16 * (ni >> 1) + pi_col(g, ni & 1);
+
+  // accumulator (mi, ni, q) is C element (a_row[mi][q>>1], pi(2t + (q&1)))
+  double acc[TM_MI][TM_NI][4];
+#pragma unroll
+  for (int mi = 0; mi < TM_MI; mi++)
+#pragma unroll
+    for (int ni = 0; ni < TM_NI; ni++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        if (ACC) {
+          const int64_t row = m0 + a_row[mi][q >> 1];
+          const int64_t col = n0 + wn0 + 16 * (ni >> 1) + pi_col(2 * t, ni & 1) + (q & 1);
+          acc[mi][ni][q] = (row < M && col < N) ? c[row * ldc + col] : 0.0;
+        } else {
+          acc[mi][ni][q] = 0.0;
+        }
+      }
+
+  // No block-wide barrier in the main loop: warps release a slab through its
+  // `empty` mbarrier, and thread 0 refills the slab consumed one iteration
+  // earlier (so it rarely waits), keeping STAGES-2 slabs in flight ahead.
+  for (int64_t kt = 0; kt < KT; kt++) {
+    const int stage = (int)(kt % TM_STAGES);
+    mbar_wait(&full[stage], (unsigned)((kt / TM_STAGES) & 1));
+    const unsigned char* as = base + stage * TM_STAGE_BYTES;
+    const unsigned char* bs = as + TM_A_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < TM_BK; kk += 4) {
+      double af[TM_MI][2], bf[TM_NI];
+#pragma unroll
+      for (int mi = 0; mi < TM_MI; mi++) {
+        af[mi][0] = *reinterpret_cast<const double*>(as + a_off(a_row[mi][0], kk + t));
+        af[mi][1] = *reinterpret_cast<const double*>(as + a_off(a_row[mi][1], kk + t));
+      }
+#pragma unroll
+      for (int ni = 0; ni < TM_NI; ni++)
+        bf[ni] = *reinterpret_cast<const double*>(bs + b_off(kk + t, b_col[ni]));
+#pragma unroll
+      for (int mi = 0; mi < TM_MI; mi++)
+#pragma unroll
+        for (int ni = 0; ni < TM_NI; ni++) dmma_step(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    // refill the slab of iteration kt-1 with k-slab kt-1+STAGES
+    if (tid == 0 && kt >= 1 && kt - 1 + TM_STAGES < KT) {
+      const int ps = (int)((kt - 1) % TM_STAGES);
+      mbar_wait(&empty[ps], (unsigned)(((kt - 1) / TM_STAGES) & 1));
+      issue(ps, kt - 1 + TM_STAGES);
+    }
+  }
+
+  // ---- epilogue: accumulator (q&1) of MMA column 2t -> tile columns pi(2t), pi(2t+1)
+  const bool pair_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(c) % 16 == 0);
+#pragma unroll
+  for (int mi = 0; mi < TM_MI; mi++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int64_t row = m0 + a_row[mi][h];
+      if (row >= M) continue;
+      double* crow = c + row * ldc;
+#pragma unroll
+      for (int ni = 0; ni < TM_NI; ni++) {
+        const int64_t col = n0 + wn0 + 16 * (ni >> 1) + pi_col(2 * t, ni & 1);
+        if (pair_ok && col + 1 < N) {
+          *reinterpret_cast<double2*>(crow + col) =
+              make_double2(acc[mi][ni][2 * h], acc[mi][ni][2 * h + 1]);
+        } else {
+          if (col < N) crow[col] = acc[mi][ni][2 * h];
+          if (col + 1 < N) crow[col + 1] = acc[mi][ni][2 * h + 1];
+        }
+      }
+    }
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return EncodeTiled(nullptr);
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// row-major rows x cols matrix with row stride ld (elements), box box_rows x 16
+bool make_map(CUtensorMap* map, const double* ptr, int64_t rows, int64_t cols, int64_t ld,
+              int box_rows) {
+  EncodeTiled enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool dmma_tma_eligible(const Problem& p) {
+  // TMA: 16-byte aligned bases and row strides, 32-bit coordinates.  The
+  // tensor map's global strides must also be below 2^40 bytes.
+  return p.lda % 2 == 0 && p.ldb % 2 == 0 &&
+         reinterpret_cast<uintptr_t>(p.a) % 16 == 0 && reinterpret_cast<uintptr_t>(p.b) % 16 == 0 &&
+         p.M < (int64_t(1) << 31) && p.N < (int64_t(1) << 31) && p.K < (int64_t(1) << 31) &&
+         p.lda < (int64_t(1) << 36) && p.ldb < (int64_t(1) << 36) && encoder() != nullptr;
+}
+
+cudaError_t launch_dmma_tma(const Problem& p) {
+  CUtensorMap map_a, map_b;
+  if (!make_map(&map_a, static_cast<const double*>(p.a), p.M, p.K, p.lda, TM_BM) ||
+      !make_map(&map_b, static_cast<const double*>(p.b), p.K, p.N, p.ldb, TM_BK))
+    return cudaErrorInvalidValue;
+  auto kern = p.accumulate ? dmma_tma_kernel<true> : dmma_tma_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TM_SMEM);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles_m = (p.M + TM_BM - 1) / TM_BM, tiles_n = (p.N + TM_BN - 1) / TM_BN;
+  const int64_t tiles = tiles_m * tiles_n;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)tiles, TM_THREADS, TM_SMEM, p.stream>>>(
+      static_cast<double*>(p.c), p.M, p.N, p.K, p.ldc, tiles_m, tiles_n, map_a, map_b);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace moa

@@ -32,6 +32,9 @@ cudaError_t launch_outer(const Problem& p);
 cudaError_t launch_fill(const Problem& p);
 // (multiply, add) on float64: FP64 tensor-core (DMMA) kernel.  dmma.cu
 cudaError_t launch_dmma(const Problem& p);
+// the same product with TMA-staged operands (dmma_tma.cu); bitwise identical
+bool dmma_tma_eligible(const Problem& p);
+cudaError_t launch_dmma_tma(const Problem& p);
 // everything else: CUDA-core semiring kernel (exact compare-select fold, plus
 // the device-checked FMNMX3 fast loop for add/subtract x min/max).  semiring.cu
 cudaError_t launch_semiring(const Problem& p);

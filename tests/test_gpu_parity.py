@@ -292,6 +292,46 @@ def test_dmma_tile_configs_bitwise_identical(rng):
     assert_within(full[:64 * n].cpu().numpy(), want, sum_tolerance(k, a, b))
 
 
+def test_dmma_tma_edges_bitwise_equal_cp_async_path(rng):
+    """The TMA-staged kernel (dmma_tma.cu, taken when >= 148 64x128 tiles and
+    even row strides) against the cp.async kernels on row subsets: ragged M and
+    N, K not a multiple of the 16-deep slab (TMA zero fill), round-robin rows
+    (lda = K*step), and accumulate mode — all bitwise equal, and within the
+    north_star tolerance of the reference."""
+    torch = _torch()
+    m, k, n = 1000, 38, 2102
+    a = rng.random(m * k) * 2 - 1
+    b = rng.random(k * n) * 2 - 1
+    init = rng.random(m * n) * 2 - 1
+    ad, bd = _dev(a), _dev(b)
+    plan = plan_inner((m, k), (k, n))
+    for acc in (False, True):
+        full = _dev(init.copy())
+        launch(plan, full, ad, bd, moa.MUL_ADD, accumulate=acc)
+        full = full.cpu().numpy()
+        for r0, r1 in ((0, 64), (936, 1000), (400, 650)):
+            sub = _dev(init[r0 * n:r1 * n].copy())
+            launch(plan_inner((r1 - r0, k), (k, n)), sub, ad[r0 * k:r1 * k], bd, moa.MUL_ADD,
+                   accumulate=acc)
+            assert_bits_equal(sub.cpu().numpy(), full[r0 * n:r1 * n], f"acc={acc} rows {r0}:{r1}")
+        want = oracle.product(a, b, m, k, n, MUL, ADD, res=init.copy() if acc else None)
+        tol = sum_tolerance(k, a, b) + (k + 1) * 2.0**-52 * float(np.max(np.abs(init)))
+        assert_within(full, want, tol, f"acc={acc}")
+    # every other row (lda = 2K, ldc = 2N), as execute_parallel's round-robin
+    # row sets give
+    big = rng.random(2 * m * k) * 2 - 1
+    res = torch.zeros(2 * m * n, dtype=torch.float64, device="cuda")
+    launch(plan_inner((2 * m, k), (k, n)), res, _dev(big), bd, moa.MUL_ADD, start=1, step=2)
+    got = res.cpu().numpy().reshape(2 * m, n)
+    assert not got[0::2].any()
+    rows = np.ascontiguousarray(big.reshape(2 * m, k)[1::2]).ravel()
+    ref = torch.empty(64 * n, dtype=torch.float64, device="cuda")
+    launch(plan_inner((64, k), (k, n)), ref, _dev(rows[:64 * k]), bd, moa.MUL_ADD)
+    assert_bits_equal(got[1::2][:64].ravel(), ref.cpu().numpy())
+    assert_within(got[1::2].ravel(), oracle.product(rows, b, m, k, n, MUL, ADD),
+                  sum_tolerance(k, rows, b))
+
+
 def test_tropical_fast_and_exact_loops_agree(rng):
     """float32 (add|subtract, min|max): the FMNMX3 loop (clean data) and the
     compare-select loop (data with NaN/-0) both equal the reference."""

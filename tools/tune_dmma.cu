@@ -5,6 +5,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
 //        -I include -o tools/tune_dmma tools/tune_dmma.cu
 #include "../paper_0907_0792_b200/csrc/dmma.cu"
+#include "../paper_0907_0792_b200/csrc/dmma_tma.cu"
 
 #include <cstdio>
 #include <vector>
@@ -45,6 +46,31 @@ double run_cfg(const moa::Problem& p, int reps) {
   return best;
 }
 
+void trial_tma(const Shape& sh, double* A, double* B, double* C, double* Cref,
+               unsigned long long* d_cnt) {
+  moa::Problem p{MOA_DTYPE_F64, C, A, B, sh.M, sh.K, sh.N, sh.K, sh.N, sh.N, 2, 0, false, 0};
+  if (!moa::dmma_tma_eligible(p)) { printf("{\"cfg\": \"tma\", \"eligible\": false}\n"); return; }
+  cudaEvent_t s, e;
+  CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
+  CK(moa::launch_dmma_tma(p));
+  CK(cudaDeviceSynchronize());
+  const int reps = sh.M * sh.N * sh.K > (1ll << 36) ? 2 : 10;
+  float best = 1e30f;
+  for (int r = 0; r < reps; r++) {
+    CK(cudaEventRecord(s)); CK(moa::launch_dmma_tma(p)); CK(cudaEventRecord(e));
+    CK(cudaEventSynchronize(e));
+    float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
+  }
+  unsigned long long diff = 0;
+  CK(cudaMemset(d_cnt, 0, 8));
+  count_diff<<<1184, 256>>>(C, Cref, (size_t)sh.M * sh.N, d_cnt);
+  CK(cudaMemcpy(&diff, d_cnt, 8, cudaMemcpyDeviceToHost));
+  const double tf = 2.0 * sh.M * sh.N * sh.K / (best * 1e-3) / 1e12;
+  printf("{\"shape\": \"%s\", \"cfg\": \"tma_64x128_s4_2cta\", \"ms\": %.4f, \"tflops\": %.2f, "
+         "\"frac_of_36.96\": %.4f, \"bit_diffs_vs_first\": %llu}\n", sh.name, best, tf, tf / 36.96, diff);
+  fflush(stdout);
+}
+
 template <class Cfg>
 void trial(const char* cname, const Shape& sh, double* A, double* B, double* C, double* Cref,
            unsigned long long* d_cnt, bool first) {
@@ -67,7 +93,7 @@ void trial(const char* cname, const Shape& sh, double* A, double* B, double* C, 
 
 int main() {
   std::vector<Shape> shapes = {{"c4", 16384, 16384, 16384}, {"c3", 32768, 256, 4096},
-                               {"c1", 256, 256, 256}};
+                               {"c1", 256, 256, 256}, {"odd", 1000, 333, 777}};
   for (const Shape& sh : shapes) {
     double *A, *B, *C, *Cref;
     unsigned long long* d_cnt;
@@ -76,19 +102,8 @@ int main() {
     CK(cudaMalloc(&d_cnt, 8));
     fill_uniform<<<1184, 256>>>(A, sh.M * sh.K, 1); fill_uniform<<<1184, 256>>>(B, sh.K * sh.N, 2);
     using namespace moa;
-    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2>>("64x128_w32x32_s4_bk16_2cta", sh, A, B, C, Cref, d_cnt, true);
-    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, true>>("64x128_..._prefetch", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>>("64x128_..._group16", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 4>>("64x128_..._group4", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, true, 16>>("64x128_..._prefetch_group16", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 128, 32, 32, 3, 32, 2, true>>("64x128_s3_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<64, 64, 32, 32, 3, 16, 3, true>>("64x64_s3_3cta_prefetch", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<32, 32, 16, 16, 3, 32>>("32x32_w16x16_s3_bk32", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<32, 32, 16, 16, 3, 32, 1, true>>("32x32_w16x16_s3_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
-    if (sh.K <= 512) {
-      trial<DmmaCfg<16, 16, 16, 16, 8, 32, 1, true>>("16x16_w16x16_s8_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
-      trial<DmmaCfg<16, 32, 16, 16, 8, 32, 1, true>>("16x32_w16x16_s8_bk32_prefetch", sh, A, B, C, Cref, d_cnt, false);
-    }
+    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>>("64x128_s4_2cta_g16", sh, A, B, C, Cref, d_cnt, true);
+    trial_tma(sh, A, B, C, Cref, d_cnt);
     CK(cudaFree(A)); CK(cudaFree(B)); CK(cudaFree(C)); CK(cudaFree(Cref)); CK(cudaFree(d_cnt));
   }
   return 0;
