@@ -18,9 +18,8 @@
 // the epilogue writes each accumulator pair to the relabelled (still
 // contiguous) positions.  Each C element still accumulates k in ascending
 // 4-wide DMMA steps from k = 0, so the bits equal every dmma.cu configuration.
-#include <cuda.h>
-
 #include "moa_common.cuh"
+#include "tma.cuh"
 #include "moa_kernels.h"
 #include "../../include/moa_b200.h"
 
@@ -38,37 +37,11 @@ constexpr size_t TM_SMEM = (size_t)TM_STAGES * TM_STAGE_BYTES + 1024 /*align*/ +
 constexpr int TM_WARPS = TM_THREADS / 32;
 constexpr int TM_GROUP_M = 16;
 
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
-      : "memory");
-}
+using tma::load_2d;
+using tma::mbar_arrive;
+using tma::mbar_expect_tx;
+using tma::mbar_init;
+using tma::mbar_wait;
 
 __device__ __forceinline__ void dmma_step(double (&d)[4], double a0, double a1, double b0) {
   asm volatile(
@@ -102,7 +75,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   // swizzle-128B destinations must be 1024-byte aligned
   // (offset from tm_raw rather than integer rounding of the pointer, so the
   // compiler keeps the shared address space: LDS, not generic LD)
-  unsigned char* base = tm_raw + ((1024u - (smem_addr(tm_raw) & 1023u)) & 1023u);
+  unsigned char* base = tma::align1k(tm_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + TM_STAGES * TM_STAGE_BYTES);
   uint64_t* empty = full + TM_STAGES;  // one arrival per warp when it is done with a slab
 
@@ -123,7 +96,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], TM_WARPS);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma::mbar_init_fence();
   }
   __syncthreads();
 
@@ -131,10 +104,10 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   auto issue = [&](int stage, int64_t kt) {  // one thread
     unsigned char* st = base + stage * TM_STAGE_BYTES;
     mbar_expect_tx(&full[stage], TM_STAGE_BYTES);
-    tma_load_2d(st, &map_a, (int)(kt * TM_BK), (int)m0, &full[stage]);
+    load_2d(st, &map_a, (int)(kt * TM_BK), (int)m0, &full[stage]);
 #pragma unroll
     for (int j = 0; j < TM_BN / 16; j++)
-      tma_load_2d(st + TM_A_BYTES + j * 2048, &map_b, (int)(n0 + 16 * j), (int)(kt * TM_BK),
+      load_2d(st + TM_A_BYTES + j * 2048, &map_b, (int)(n0 + 16 * j), (int)(kt * TM_BK),
                   &full[stage]);
   };
   if (tid == 0) {
@@ -228,38 +201,6 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     }
 }
 
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiled encoder() {
-  static EncodeTiled fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return EncodeTiled(nullptr);
-    return reinterpret_cast<EncodeTiled>(p);
-  }();
-  return fn;
-}
-
-// row-major rows x cols matrix with row stride ld (elements), box box_rows x 16
-bool make_map(CUtensorMap* map, const double* ptr, int64_t rows, int64_t cols, int64_t ld,
-              int box_rows) {
-  EncodeTiled enc = encoder();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 }  // namespace
 
 bool dmma_tma_eligible(const Problem& p) {
@@ -268,13 +209,13 @@ bool dmma_tma_eligible(const Problem& p) {
   return p.lda % 2 == 0 && p.ldb % 2 == 0 &&
          reinterpret_cast<uintptr_t>(p.a) % 16 == 0 && reinterpret_cast<uintptr_t>(p.b) % 16 == 0 &&
          p.M < (int64_t(1) << 31) && p.N < (int64_t(1) << 31) && p.K < (int64_t(1) << 31) &&
-         p.lda < (int64_t(1) << 36) && p.ldb < (int64_t(1) << 36) && encoder() != nullptr;
+         p.lda < (int64_t(1) << 36) && p.ldb < (int64_t(1) << 36) && tensor_maps_available();
 }
 
 cudaError_t launch_dmma_tma(const Problem& p) {
   CUtensorMap map_a, map_b;
-  if (!make_map(&map_a, static_cast<const double*>(p.a), p.M, p.K, p.lda, TM_BM) ||
-      !make_map(&map_b, static_cast<const double*>(p.b), p.K, p.N, p.ldb, TM_BK))
+  if (!make_tensor_map_2d(&map_a, p.a, 8, p.M, p.K, p.lda, TM_BM, 16, true) ||
+      !make_tensor_map_2d(&map_b, p.b, 8, p.K, p.N, p.ldb, TM_BK, 16, true))
     return cudaErrorInvalidValue;
   auto kern = p.accumulate ? dmma_tma_kernel<true> : dmma_tma_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TM_SMEM);

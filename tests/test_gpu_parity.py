@@ -332,10 +332,12 @@ def test_dmma_tma_edges_bitwise_equal_cp_async_path(rng):
                   sum_tolerance(k, rows, b))
 
 
-def test_tropical_fast_and_exact_loops_agree(rng):
-    """float32 (add|subtract, min|max): the FMNMX3 loop (clean data) and the
-    compare-select loop (data with NaN/-0) both equal the reference."""
-    m, k, n = 257, 131, 300  # odd K: the last k of the last tile takes the scalar tail
+@pytest.mark.parametrize("mkn", [(257, 131, 300),   # odd K, unaligned rows: cp.async kernel
+                                 (1000, 132, 1004)])  # 16-byte rows: TMA-staged kernel
+def test_tropical_fast_and_exact_loops_agree(mkn, rng):
+    """float32 (add|subtract, min|max): the VIMNMX3 / FMNMX3 loops (clean data)
+    and the compare-select loop (data with NaN/-0) all equal the reference."""
+    m, k, n = mkn  # odd K: the last k of the last tile takes the scalar tail
     for comb in ("add", "subtract"):
         for red in ("min", "max"):
             ops = op_pair(comb, red)
@@ -358,6 +360,29 @@ def test_tropical_fast_and_exact_loops_agree(rng):
                                 MoaArray((k, n), bb, dtype=np.float32), ops).data
                 assert got.dtype == np.float32
                 assert_bits_equal(got, want, f"{ops} poison={poison}")
+
+
+def test_tropical_tma_strided_rows_odd_k(rng):
+    """Round-robin row sets (lda = K*step) keep the TMA-staged tropical kernel
+    eligible with an odd K, so its lone-k tail runs; bitwise vs the reference."""
+    torch = _torch()
+    m, k, n, step = 400, 131, 260, 4
+    for comb, red in (("add", "min"), ("subtract", "max")):
+        ops = op_pair(comb, red)
+        c, r = ops.codes()
+        a = rng.random(step * m * k, dtype=np.float32) * np.float32(100)
+        b = rng.random(k * n, dtype=np.float32) * np.float32(100)
+        for shift in (0.0, 50.0):  # non-negative sums (VIMNMX3) and signed (FMNMX3)
+            aa = a - np.float32(shift)
+            res = torch.zeros(step * m * n, dtype=torch.float32, device="cuda")
+            # start 0: the first row stays 16-byte aligned (TMA base requirement)
+            launch(plan_inner((step * m, k), (k, n)), res, _dev(aa), _dev(b), ops, start=0,
+                   step=step)
+            got = res.cpu().numpy().reshape(step * m, n)
+            rows = np.ascontiguousarray(aa.reshape(step * m, k)[0::step]).ravel()
+            want = oracle.product(rows, b, m, k, n, c, r).astype(np.float32)
+            assert_bits_equal(got[0::step].ravel(), want, f"{ops} shift={shift}")
+            assert not np.delete(got, np.s_[0::step], axis=0).any()
 
 
 def test_launch_counter_advances():

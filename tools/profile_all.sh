@@ -15,8 +15,10 @@ echo "ncu c2 rc=$?"
 for C in c4 c5 c3 c1; do
   CMDC="python bench.py --config $C --steps 1 --warmup 3 --no-cpu"
   $CMDC > $OUT/plain_${C}_$TAG.log 2>&1 || { echo "plain $C failed"; continue; }
-  case $C in c5) K="tropical_kernel<0, 2, 2";; *) K=dmma_kernel;; esac
-  ncu --set full --clock-control none --import-source on -k "regex:$K" -s 1 -c 1 \
+  # c5 launches the VIMNMX3 and FMNMX3 specialisations per product (the second
+  # exits at once): skip the first product's two to land on the working one
+  case $C in c5) K=tropical; S=2;; *) K=dmma; S=1;; esac
+  ncu --set full --clock-control none --import-source on -k "regex:$K" -s $S -c 1 \
       -o $OUT/prof_${C}_$TAG $CMDC > $OUT/ncu_${C}_$TAG.log 2>&1
   echo "ncu $C rc=$?"
 done

@@ -4,6 +4,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
 //        -o tools/tune_semiring tools/tune_semiring.cu
 #include "../paper_0907_0792_b200/csrc/semiring_impl.cuh"
+#include "../paper_0907_0792_b200/csrc/tma.cu"
 
 #include <cstdio>
 
@@ -53,6 +54,33 @@ void trial_tropical(const moa::Problem& p0, float* out, float* ref, unsigned* sp
   fflush(stdout);
 }
 
+void trial_tma(const moa::Problem& p0, float* out, float* ref, unsigned* special,
+               unsigned long long* cnt) {
+  moa::Problem p = p0;
+  p.c = out;
+  if (!moa::tropical_tma_eligible(p)) { printf("{\"kernel\": \"tropical_tma\", \"eligible\": false}\n"); return; }
+  cudaEvent_t s, e;
+  CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
+  CK(cudaMemset(out, 0, (size_t)p.M * p.N * 4));
+  CK((moa::tropical_tma_launch<0, 2, 2>(p, special)));
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 2; r++) {
+    CK(cudaEventRecord(s));
+    CK((moa::tropical_tma_launch<0, 2, 2>(p, special)));
+    CK(cudaEventRecord(e)); CK(cudaEventSynchronize(e));
+    float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
+  }
+  unsigned long long diff = 0;
+  CK(cudaMemset(cnt, 0, 8));
+  count_diff<<<1184, 256>>>(out, ref, (size_t)p.M * p.N, cnt);
+  CK(cudaMemcpy(&diff, cnt, 8, cudaMemcpyDeviceToHost));
+  const double pairs = (double)p.M * p.N * p.K;
+  printf("{\"kernel\": \"tropical_tma\", \"M\": %ld, \"K\": %ld, \"N\": %ld, \"ms\": %.3f, \"Gpairs_s\": %.1f, \"frac_of_24475\": %.4f, \"bit_diffs\": %llu}\n",
+         (long)p.M, (long)p.K, (long)p.N, best, pairs / (best * 1e-3) / 1e9, pairs / (best * 1e-3) / 1e9 / 24475.4, diff);
+  fflush(stdout);
+}
+
 template <int TM, int TN, int MINB>
 void trial(const moa::Problem& p0, float* out, float* ref, unsigned* special, unsigned long long* cnt) {
   moa::Problem p = p0;
@@ -94,6 +122,10 @@ int main() {
   moa::Problem p{MOA_DTYPE_F32, ref, a, b, n, n, n, n, n, n, 0, 2, false, 0};
   trial<8, 8, 2>(p, ref, ref, special, cnt);
   trial_tropical<false>(p, c, ref, special, cnt);
-  trial_tropical<true>(p, c, ref, special, cnt);
+  trial_tma(p, c, ref, special, cnt);
+  // ragged shape: K odd (lone-k tail), M/N not tile multiples
+  moa::Problem q{MOA_DTYPE_F32, ref, a, b, 1000, 1001, 1004, 1004, 1004, 1004, 0, 2, false, 0};
+  CK((moa::tropical_launch<0, 2, 2, false>(q, special)));
+  trial_tma(q, c, ref, special, cnt);
   return 0;
 }
