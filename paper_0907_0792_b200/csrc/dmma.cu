@@ -277,9 +277,11 @@ cudaError_t launch_dmma(const Problem& p) {
   // all configurations give identical bits (k order is fixed), so the choice
   // only has to fill the 148 SMs
   auto tiles = [&](int bm, int bn) { return ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn); };
-  // TMA-staged 64x128 kernel (dmma_tma.cu): 93% of the DMMA peak on c4 vs
-  // 89% for the cp.async one (profiles/r01_tune_dmma_tma.jsonl)
-  if (tiles(64, 128) >= kNumSMs && dmma_tma_eligible(p)) return launch_dmma_tma(p);
+  // TMA-staged 64x64 kernel (dmma_tma.cu) once it fills the SMs: 96.9% of the
+  // DMMA peak at c4 vs 88.9% for the cp.async kernels
+  // (profiles/r01_tune_dmma_tma_cfgs.jsonl); below that the small cp.async
+  // tiles win (more CTAs)
+  if (tiles(64, 64) >= kNumSMs && dmma_tma_eligible(p)) return launch_dmma_tma(p);
   if (tiles(64, 128) >= 2 * kNumSMs) return dmma_dispatch<CfgLarge>(p);
   if (tiles(64, 64) >= kNumSMs) return dmma_dispatch<CfgMedium>(p);
   return dmma_dispatch<CfgSmall>(p);

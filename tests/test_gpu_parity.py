@@ -274,26 +274,39 @@ def test_unaligned_operands_and_odd_strides(rng):
 
 
 def test_dmma_tile_configs_bitwise_identical(rng):
-    """Large-tile (many rows) and small-tile (few rows) launches accumulate
-    in the same k order, so shared rows are bitwise equal (the GPU-count
-    determinism argument)."""
+    """Every (multiply, add) kernel configuration — TMA 64x64 (aligned, many
+    rows), cp.async 64x128 / 64x64 (rows misaligned for TMA), cp.async 32x32
+    (few rows) — accumulates in the same k order, so shared rows are bitwise
+    equal (the GPU-count determinism argument)."""
     torch = _torch()
     m, k, n = 4096, 300, 2048
-    a = rng.random(m * k) * 2 - 1
+    a = rng.random(m * k + 1) * 2 - 1
     b = rng.random(k * n) * 2 - 1
-    ad, bd = _dev(a), _dev(b)
-    full = torch.empty(m * n, dtype=torch.float64, device="cuda")
-    launch(plan_inner((m, k), (k, n)), full, ad, bd, moa.MUL_ADD)
-    for r0, r1 in ((0, 64), (1000, 1130), (1000, 1400), (4000, 4096)):  # small, small, medium, small
-        sub = torch.empty((r1 - r0) * n, dtype=torch.float64, device="cuda")
-        launch(plan_inner((r1 - r0, k), (k, n)), sub, ad[r0 * k:r1 * k], bd, moa.MUL_ADD)
-        assert_bits_equal(sub.cpu().numpy(), full[r0 * n:r1 * n].cpu().numpy())
-    want = oracle.product(a[:64 * k], b, 64, k, n, MUL, ADD)
-    assert_within(full[:64 * n].cpu().numpy(), want, sum_tolerance(k, a, b))
+    bd = _dev(b)
+    outs = []
+    for shift in (0, 1):  # shift 1: 8-byte aligned A rows, TMA ineligible
+        ad = _dev(a)[shift:shift + m * k]
+        full = torch.empty(m * n, dtype=torch.float64, device="cuda")
+        launch(plan_inner((m, k), (k, n)), full, ad, bd, moa.MUL_ADD)
+        full = full.cpu().numpy()
+        # rows: 64 (small), 130 (small), 400 (TMA / cp.async medium), 96 (small)
+        for r0, r1 in ((0, 64), (1000, 1130), (1000, 1400), (4000, 4096)):
+            sub = torch.empty((r1 - r0) * n, dtype=torch.float64, device="cuda")
+            launch(plan_inner((r1 - r0, k), (k, n)), sub, ad[r0 * k:r1 * k], bd, moa.MUL_ADD)
+            assert_bits_equal(sub.cpu().numpy(), full[r0 * n:r1 * n], f"shift={shift} {r0}:{r1}")
+        want = oracle.product(a[shift:shift + 64 * k], b, 64, k, n, MUL, ADD)
+        assert_within(full[:64 * n], want, sum_tolerance(k, a, b))
+        outs.append(full)
+    # same A values at both alignments except the one-element shift: compare
+    # the aligned run on a[1:] through a copy instead
+    ad = _dev(np.ascontiguousarray(a[1:1 + m * k]))
+    again = torch.empty(m * n, dtype=torch.float64, device="cuda")
+    launch(plan_inner((m, k), (k, n)), again, ad, bd, moa.MUL_ADD)
+    assert_bits_equal(again.cpu().numpy(), outs[1], "TMA vs cp.async large tiles")
 
 
 def test_dmma_tma_edges_bitwise_equal_cp_async_path(rng):
-    """The TMA-staged kernel (dmma_tma.cu, taken when >= 148 64x128 tiles and
+    """The TMA-staged kernel (dmma_tma.cu, taken when >= 148 64x64 tiles and
     even row strides) against the cp.async kernels on row subsets: ragged M and
     N, K not a multiple of the 16-deep slab (TMA zero fill), round-robin rows
     (lda = K*step), and accumulate mode — all bitwise equal, and within the

@@ -6,6 +6,7 @@
 //        -I include -o tools/tune_dmma tools/tune_dmma.cu
 #include "../paper_0907_0792_b200/csrc/dmma.cu"
 #include "../paper_0907_0792_b200/csrc/dmma_tma.cu"
+#include "../paper_0907_0792_b200/csrc/tma.cu"
 
 #include <cstdio>
 #include <vector>
@@ -46,18 +47,19 @@ double run_cfg(const moa::Problem& p, int reps) {
   return best;
 }
 
-void trial_tma(const Shape& sh, double* A, double* B, double* C, double* Cref,
+template <class Cfg>
+void trial_tma(const char* name, const Shape& sh, double* A, double* B, double* C, double* Cref,
                unsigned long long* d_cnt) {
   moa::Problem p{MOA_DTYPE_F64, C, A, B, sh.M, sh.K, sh.N, sh.K, sh.N, sh.N, 2, 0, false, 0};
   if (!moa::dmma_tma_eligible(p)) { printf("{\"cfg\": \"tma\", \"eligible\": false}\n"); return; }
   cudaEvent_t s, e;
   CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
-  CK(moa::launch_dmma_tma(p));
+  CK(moa::dmma_tma_launch<Cfg>(p));
   CK(cudaDeviceSynchronize());
   const int reps = sh.M * sh.N * sh.K > (1ll << 36) ? 2 : 10;
   float best = 1e30f;
   for (int r = 0; r < reps; r++) {
-    CK(cudaEventRecord(s)); CK(moa::launch_dmma_tma(p)); CK(cudaEventRecord(e));
+    CK(cudaEventRecord(s)); CK(moa::dmma_tma_launch<Cfg>(p)); CK(cudaEventRecord(e));
     CK(cudaEventSynchronize(e));
     float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
   }
@@ -66,8 +68,8 @@ void trial_tma(const Shape& sh, double* A, double* B, double* C, double* Cref,
   count_diff<<<1184, 256>>>(C, Cref, (size_t)sh.M * sh.N, d_cnt);
   CK(cudaMemcpy(&diff, d_cnt, 8, cudaMemcpyDeviceToHost));
   const double tf = 2.0 * sh.M * sh.N * sh.K / (best * 1e-3) / 1e12;
-  printf("{\"shape\": \"%s\", \"cfg\": \"tma_64x128_s4_2cta\", \"ms\": %.4f, \"tflops\": %.2f, "
-         "\"frac_of_36.96\": %.4f, \"bit_diffs_vs_first\": %llu}\n", sh.name, best, tf, tf / 36.96, diff);
+  printf("{\"shape\": \"%s\", \"cfg\": \"tma_%s\", \"ms\": %.4f, \"tflops\": %.2f, "
+         "\"frac_of_36.96\": %.4f, \"bit_diffs_vs_first\": %llu}\n", sh.name, name, best, tf, tf / 36.96, diff);
   fflush(stdout);
 }
 
@@ -92,8 +94,8 @@ void trial(const char* cname, const Shape& sh, double* A, double* B, double* C, 
 }
 
 int main() {
-  std::vector<Shape> shapes = {{"c4", 16384, 16384, 16384}, {"c3", 32768, 256, 4096},
-                               {"c1", 256, 256, 256}, {"odd", 1000, 333, 777}};
+  std::vector<Shape> shapes = {{"m1k", 1024, 1024, 1024}, {"m2k", 2048, 512, 2048},
+                               {"c3", 32768, 256, 4096}, {"c4", 16384, 16384, 16384}};
   for (const Shape& sh : shapes) {
     double *A, *B, *C, *Cref;
     unsigned long long* d_cnt;
@@ -103,7 +105,13 @@ int main() {
     fill_uniform<<<1184, 256>>>(A, sh.M * sh.K, 1); fill_uniform<<<1184, 256>>>(B, sh.K * sh.N, 2);
     using namespace moa;
     trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>>("64x128_s4_2cta_g16", sh, A, B, C, Cref, d_cnt, true);
-    trial_tma(sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaLarge>("64x128_s4", sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaCfg<64, 64, 32, 32, 4, 2, 8>>("64x64_s4_2cta", sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaCfg<64, 64, 32, 32, 4, 3, 8>>("64x64_s4_3cta", sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaCfg<64, 64, 32, 32, 4, 3, 16>>("64x64_s4_3cta_g16", sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaCfg<64, 64, 32, 32, 6, 2, 8>>("64x64_s6_2cta", sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaCfg<128, 64, 32, 32, 4, 2, 8>>("128x64_s4_2cta", sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaCfg<64, 64, 32, 32, 3, 4, 8>>("64x64_s3_4cta", sh, A, B, C, Cref, d_cnt);
     CK(cudaFree(A)); CK(cudaFree(B)); CK(cudaFree(C)); CK(cudaFree(Cref)); CK(cudaFree(d_cnt));
   }
   return 0;
