@@ -256,10 +256,14 @@ cudaError_t dmma_launch(const Problem& p) {
 //        groups of 16 row tiles (tools/traffic_dmma.cu: 83 GB of DRAM reads per c4
 //        launch vs 94 GB for 8, same time)
 // medium: 64x64 CTA, 4 warps of 32x32, 3 stages, 3 CTAs/SM
-// small: 32x32 CTA, 4 warps of 16x16, BK=32 (few k-tile round trips; c1-sized problems)
+// small: 32x32 CTA, 4 warps of 16x16, BK=32 (few k-tile round trips)
+// tiny: 16x32 CTA, 4 warps of 16x8: the most warps for problems that give
+//       fewer than 148 small tiles (c1: 8.7 vs 10.8 us; one warp already
+//       saturates its sub-partition's DMMA pipe, tools/mb_dmma_latency.cu)
 using CfgLarge = DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>;
 using CfgMedium = DmmaCfg<64, 64, 32, 32, 3, 16, 3>;
 using CfgSmall = DmmaCfg<32, 32, 16, 16, 3, 32, 1>;
+using CfgTiny = DmmaCfg<16, 32, 16, 8, 3, 32, 1>;
 
 template <class Cfg>
 cudaError_t dmma_dispatch(const Problem& p) {
@@ -284,7 +288,8 @@ cudaError_t launch_dmma(const Problem& p) {
   if (tiles(64, 64) >= kNumSMs && dmma_tma_eligible(p)) return launch_dmma_tma(p);
   if (tiles(64, 128) >= 2 * kNumSMs) return dmma_dispatch<CfgLarge>(p);
   if (tiles(64, 64) >= kNumSMs) return dmma_dispatch<CfgMedium>(p);
-  return dmma_dispatch<CfgSmall>(p);
+  if (tiles(32, 32) >= kNumSMs) return dmma_dispatch<CfgSmall>(p);
+  return dmma_dispatch<CfgTiny>(p);
 }
 
 }  // namespace moa

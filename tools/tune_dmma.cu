@@ -94,8 +94,7 @@ void trial(const char* cname, const Shape& sh, double* A, double* B, double* C, 
 }
 
 int main() {
-  std::vector<Shape> shapes = {{"m1k", 1024, 1024, 1024}, {"m2k", 2048, 512, 2048},
-                               {"c3", 32768, 256, 4096}, {"c4", 16384, 16384, 16384}};
+  std::vector<Shape> shapes = {{"c1", 256, 256, 256}, {"c1b", 256, 256, 256}};
   for (const Shape& sh : shapes) {
     double *A, *B, *C, *Cref;
     unsigned long long* d_cnt;
@@ -104,14 +103,14 @@ int main() {
     CK(cudaMalloc(&d_cnt, 8));
     fill_uniform<<<1184, 256>>>(A, sh.M * sh.K, 1); fill_uniform<<<1184, 256>>>(B, sh.K * sh.N, 2);
     using namespace moa;
-    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>>("64x128_s4_2cta_g16", sh, A, B, C, Cref, d_cnt, true);
-    trial_tma<moa::TmaLarge>("64x128_s4", sh, A, B, C, Cref, d_cnt);
-    trial_tma<moa::TmaCfg<64, 64, 32, 32, 4, 2, 8>>("64x64_s4_2cta", sh, A, B, C, Cref, d_cnt);
-    trial_tma<moa::TmaCfg<64, 64, 32, 32, 4, 3, 8>>("64x64_s4_3cta", sh, A, B, C, Cref, d_cnt);
-    trial_tma<moa::TmaCfg<64, 64, 32, 32, 4, 3, 16>>("64x64_s4_3cta_g16", sh, A, B, C, Cref, d_cnt);
-    trial_tma<moa::TmaCfg<64, 64, 32, 32, 6, 2, 8>>("64x64_s6_2cta", sh, A, B, C, Cref, d_cnt);
-    trial_tma<moa::TmaCfg<128, 64, 32, 32, 4, 2, 8>>("128x64_s4_2cta", sh, A, B, C, Cref, d_cnt);
-    trial_tma<moa::TmaCfg<64, 64, 32, 32, 3, 4, 8>>("64x64_s3_4cta", sh, A, B, C, Cref, d_cnt);
+    trial<DmmaCfg<32, 32, 16, 16, 3, 32, 1>>("32x32_small", sh, A, B, C, Cref, d_cnt, true);
+    trial<DmmaCfg<16, 32, 16, 8, 3, 32, 1>>("16x32_w16x8", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<16, 32, 16, 8, 4, 32, 1>>("16x32_w16x8_s4", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<16, 32, 16, 8, 2, 32, 1>>("16x32_w16x8_s2", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<16, 32, 16, 8, 3, 64, 1>>("16x32_w16x8_bk64", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<16, 32, 16, 8, 5, 16, 1>>("16x32_w16x8_bk16_s5", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<16, 32, 16, 8, 3, 32, 1, true>>("16x32_w16x8_pf", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<16, 64, 16, 8, 3, 32, 1>>("16x64_w16x8", sh, A, B, C, Cref, d_cnt, false);
     CK(cudaFree(A)); CK(cudaFree(B)); CK(cudaFree(C)); CK(cudaFree(Cref)); CK(cudaFree(d_cnt));
   }
   return 0;
