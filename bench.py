@@ -8,7 +8,9 @@ result, metric "outer-product GB/s" (algorithmic bytes 8*(M*N + M + N) per unit)
 ``--config c1|c3|c4`` measure the (+,x) inner products in GFLOP/s, ``c5`` the
 tropical product in G pairs/s.  At N=1 the default run also measures c1, c3, c4
 and c5 device-resident (key "inner"), so one line carries both halves of the
-metric ("inner-product GFLOP/s & outer-product GB/s ... % of roofline").
+metric ("inner-product GFLOP/s & outer-product GB/s ... % of roofline"); at
+N>1 "inner" holds c4 and c5 with their result rows sharded over the ranks
+(BASELINE configs 4-5: B broadcast inside every step, strong scaling).
 
 A step is one pass of the product over one unit of synthetic input:
 * ``value``: inputs resident in HBM; per step, rank 0's B is broadcast (NCCL,
@@ -550,7 +552,8 @@ def main() -> None:
             "data": "synthetic (seeded generators of SURVEY.md §8d; no public dataset)",
             "config": {"workload": f"{w.key}: {w.description}", "M": m, "K": k, "N": n,
                        "rows_per_rank": rows_range[1] - rows_range[0],
-                       "parallelism": f"row-sharded x{world}, B broadcast (NCCL)" if world > 1
+                       "parallelism": f"row-sharded x{world}, B broadcast ({dist.get_backend().upper()})"
+                       if world > 1
                        else "single GPU",
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "cuda_graph": bool(dev.get("graph"))},
@@ -576,6 +579,31 @@ def main() -> None:
                           "value": round(to_unit(wi, amt, d["step_ms_total"] / st * 1e-3), 2),
                           "kernel_ms": round(d["kernel_ms_mean"], 4),
                           "roofline": roofline(wi, mi, d["kernel_ms_mean"]),
+                          "clocks": d["clocks"]}
+            del ai, bi
+        line["inner"] = inner
+
+    if world > 1 and not args.no_inner and w.key == "c2":
+        # BASELINE configs 4-5 at N GPUs: result rows sharded over the ranks, B
+        # broadcast from rank 0 inside every step (strong scaling, max over ranks)
+        from paper_0907_0792_b200.distributed import row_block
+        inner = {}
+        for key in ("c4", "c5"):
+            wi = WORKLOADS[key]
+            ai, bi = wi.generate()
+            mi = wi.mkn[0]
+            rr = row_block(mi, world, rank)
+            st = 3
+            d = measure_device(wi, rr, ai, bi, st, 3, device, world, rank)
+            t = torch.tensor([d["step_ms_total"], d["kernel_ms_mean"]], dtype=torch.float64,
+                             device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            amt = unit_amount(wi, mi)
+            inner[key] = {"metric": METRIC[key][0], "unit": METRIC[key][1], "scaling": "strong",
+                          "value": round(to_unit(wi, amt, t[0].item() / st * 1e-3), 2),
+                          "rows_per_rank": rr[1] - rr[0],
+                          "kernel_ms": round(t[1].item(), 4),
+                          "roofline": roofline(wi, rr[1] - rr[0], t[1].item()),
                           "clocks": d["clocks"]}
             del ai, bi
         line["inner"] = inner

@@ -1,0 +1,80 @@
+"""Throughput of every (dtype, combine, reduce) route at one inner-product size.
+
+Runs on a GPU box (tools; not part of the library):
+
+    python tools/route_sweep.py [--n 4096] [--out gpurun_out/route_sweep.jsonl]
+
+For each of the 4 dtypes x 24 op pairs: seeded operands of n x n (values that
+keep every route on its common path: positive for the tropical fast loops,
+small integers so integer products stay meaningful), one warm-up launch, then
+the best of 3 CUDA-event-timed launches through ``kernel.launch`` (the C ABI).
+Prints one JSON line per route with the kernel ``moa_plan_kernel`` reports and
+G pairs/s (M*K*N / time).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_0907_0792_b200 as moa  # noqa: E402
+from paper_0907_0792_b200 import _native  # noqa: E402
+from paper_0907_0792_b200.kernel import launch, native_dtype, plan_inner  # noqa: E402
+
+
+def operands(dt, n, gen):
+    if np.dtype(dt).kind == "i":
+        a = gen.integers(-1000, 1000, size=n * n).astype(dt)
+        b = gen.integers(-1000, 1000, size=n * n).astype(dt)
+    else:
+        a = (gen.random(n * n) * 100).astype(dt)
+        b = (gen.random(n * n) * 100).astype(dt)
+    return torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--out", default="gpurun_out/route_sweep.jsonl")
+    args = ap.parse_args()
+    n = args.n
+    gen = np.random.default_rng(0)
+    plan = plan_inner((n, n), (n, n))
+    lines = []
+    for dt in (np.float64, np.float32, np.int32, np.int64):
+        a, b = operands(dt, n, gen)
+        res = torch.empty(n * n, dtype=a.dtype, device="cuda")
+        for comb in moa.COMBINE_OPS:
+            for red in moa.REDUCE_OPS:
+                ops = moa.op_pair(comb, red)
+                c, r = ops.codes()
+                kern = _native.plan_kernel(native_dtype(np.dtype(dt)), n, n, n, c, r, 0)
+                launch(plan, res, a, b, ops)
+                torch.cuda.synchronize()
+                best = float("inf")
+                for _ in range(3):
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    launch(plan, res, a, b, ops)
+                    e.record()
+                    e.synchronize()
+                    best = min(best, s.elapsed_time(e))
+                rec = {"dtype": np.dtype(dt).name, "combine": comb, "reduce": red, "kernel": kern,
+                       "n": n, "ms": round(best, 4),
+                       "Gpairs_s": round(n ** 3 / (best * 1e-3) / 1e9, 1)}
+                lines.append(rec)
+                print(json.dumps(rec), flush=True)
+        del a, b, res
+        torch.cuda.empty_cache()
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text("".join(json.dumps(x) + "\n" for x in lines))
+
+
+if __name__ == "__main__":
+    main()
