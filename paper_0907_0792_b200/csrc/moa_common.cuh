@@ -61,6 +61,81 @@ template <typename T> __device__ __forceinline__ T safe_div(T x, T y) {
 // min/max are the reference's compare-and-select (ops.py:42-47), NOT fmin/fmax:
 // x if x < y else y keeps the second operand on NaN and on a +-0 tie.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Division by a reused divisor.  In the inner product every B element divides
+// a whole column of A elements, so the kernels take y = RN(1/b) once per B
+// element and form each quotient as
+//     q0 = RN(a*y), r0 = a - b*q0 (FMA), q1 = RN(q0 + r0*y), r1 = a - b*q1 (FMA, exact)
+// and ACCEPT q1 only when the exact residual proves it is the correctly
+// rounded quotient: |a - b*q1| < |b| * ulp(q1)/2, q1 not a power of two (whose
+// lower rounding interval is half as wide).  No midpoint can be a quotient of
+// two floating-point numbers, so the test is exact; operands whose exponents
+// could under/overflow any step (|a|, |b| outside [2^-400, 2^400) for double,
+// [2^-40, 2^40) for float), zeros, infinities and NaNs take the IEEE division.
+// Either way the result is RN(a/b), bit for bit (tests/test_gpu_parity.py).
+// Kernels prove a whole row of quotients at once and redo the row with the
+// IEEE division when any proof fails, so the common case has no branches.
+__device__ __forceinline__ double rcp_rn(double b) { return __drcp_rn(b); }
+__device__ __forceinline__ float rcp_rn(float b) { return __frcp_rn(b); }
+
+// operand exponent within the reciprocal path's range
+__device__ __forceinline__ bool rcp_range(double x) {
+  return ((unsigned)(__double_as_longlong(x) >> 52) & 0x7ffu) - 623u < 800u;  // [2^-400, 2^400)
+}
+__device__ __forceinline__ bool rcp_range(float x) {
+  return ((__float_as_uint(x) >> 23) & 0xffu) - 87u < 80u;  // [2^-40, 2^40)
+}
+// candidate quotient for in-range a, b with y = RN(1/b); ok &= proof that it
+// is RN(a/b).  Out-of-range operands give garbage and must not be used.
+__device__ __forceinline__ double div_candidate(double a, double b, double y, bool& ok) {
+  const double q0 = __dmul_rn(a, y);
+  const double r0 = __fma_rn(-b, q0, a);
+  const double q1 = __fma_rn(r0, y, q0);
+  const double r1 = __fma_rn(-b, q1, a);
+  const unsigned long long uq = __double_as_longlong(q1);
+  const unsigned eq = (unsigned)(uq >> 52) & 0x7ffu;  // >= 223 in range
+  const double half_ulp_b = fabs(b) * __longlong_as_double((unsigned long long)(eq - 53u) << 52);
+  ok = ok && (uq & 0xfffffffffffffull) != 0 && fabs(r1) < half_ulp_b;
+  return q1;
+}
+__device__ __forceinline__ float div_candidate(float a, float b, float y, bool& ok) {
+  const float q0 = __fmul_rn(a, y);
+  const float r0 = __fmaf_rn(-b, q0, a);
+  const float q1 = __fmaf_rn(r0, y, q0);
+  const float r1 = __fmaf_rn(-b, q1, a);
+  const unsigned uq = __float_as_uint(q1);
+  const unsigned eq = (uq >> 23) & 0xffu;  // >= 47 in range
+  const float half_ulp_b = fabsf(b) * __uint_as_float((eq - 24u) << 23);
+  ok = ok && (uq & 0x7fffffu) != 0 && fabsf(r1) < half_ulp_b;
+  return q1;
+}
+
+// Integer division by a reused divisor through yr = RN(1/double(y)).
+// q = trunc(x*yr) is exact or, when x/y is an integer, one unit short: for
+// int32 the estimate's error (< |x/y| 2^-51) is below the distance 1/|y| from
+// any non-integer x/y to the next integer.  int64 operands lose bits in the
+// conversion, so the remainder gets one more estimate (|error| < 2^13 after
+// the first).  The last unit is fixed from the exact remainder (truncating
+// division: r = 0 or sign(r) = sign(x) with |r| < |y|), and y = 0, y = -1
+// keep safe_div's results.
+template <typename T>
+__device__ __forceinline__ T idiv_by_rcp(T x, double xd, T y, double yr) {
+  using U = typename IntTraits<T>::U;
+  T q;
+  if constexpr (sizeof(T) == 8) q = T(__double2ll_rz(xd * yr));
+  else q = T(__double2int_rz(xd * yr));
+  T r = wrap_sub(x, wrap_mul(q, y));
+  if constexpr (sizeof(T) == 8) {
+    q = wrap_add(q, T(__double2ll_rz(double(r) * yr)));
+    r = wrap_sub(x, wrap_mul(q, y));
+  }
+  const T s = ((x ^ y) < 0) ? T(-1) : T(1);
+  const U ar = r < 0 ? U(0) - U(r) : U(r), ay = y < 0 ? U(0) - U(y) : U(y);
+  if (r != 0 && ((r < 0) != (x < 0))) q = wrap_sub(q, s);
+  else if (ar >= ay) q = wrap_add(q, s);
+  return y == 0 ? T(0) : (y == T(-1) ? wrap_sub(T(0), x) : q);
+}
+
 template <int C> struct CombineOp;
 template <> struct CombineOp<C_ADD> {
   static __device__ __forceinline__ double f(double x, double y) { return __dadd_rn(x, y); }

@@ -14,6 +14,8 @@
 // (4 doubles / 8 floats), loads its B chunk once, then walks its block's run
 // of consecutive rows issuing one 256-bit st.global.cs per row
 // (STG.E.EF.ENL2.256).  A warp writes 1 KiB of contiguous row per store.
+#include <type_traits>
+
 #include "moa_common.cuh"
 #include "moa_kernels.h"
 #include "../../include/moa_b200.h"
@@ -88,6 +90,42 @@ __global__ void __launch_bounds__(256) outer_vec_kernel(T* __restrict__ c, const
   T* cp = c + jv * V;
   const int64_t r0 = blockIdx.y * rows_per_block;
   const int64_t r1 = (r0 + rows_per_block) < M ? (r0 + rows_per_block) : M;
+  using A = typename AccType<T, R>::type;
+  if constexpr (C == C_DIV && sizeof(A) == 8) {
+    // the thread's V divisors are reused by every row of its run: one
+    // reciprocal each (div_candidate / idiv_by_rcp, moa_common.cuh)
+    double yv[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) {
+      const double bd = double(A(bv[q]));
+      yv[q] = (std::is_integral<A>::value || rcp_range(bd)) ? rcp_rn(bd)
+                                                            : __longlong_as_double(0x7ff8000000000000ll);
+    }
+#pragma unroll 2
+    for (int64_t i = r0; i < r1; i++) {
+      const A av = A(__ldg(a + i * lda));
+      A quo[V];
+      if constexpr (std::is_integral<A>::value) {
+        const double xd = double(av);
+#pragma unroll
+        for (int q = 0; q < V; q++) quo[q] = idiv_by_rcp(av, xd, A(bv[q]), yv[q]);
+      } else {
+        bool ok = rcp_range(av);
+#pragma unroll
+        for (int q = 0; q < V; q++) quo[q] = div_candidate(av, A(bv[q]), yv[q], ok);
+        if (!ok) {
+#pragma unroll
+          for (int q = 0; q < V; q++) quo[q] = CombineOp<C_DIV>::f(av, A(bv[q]));
+        }
+      }
+      T out[V];
+      if (ACC) ld_32B(cp + i * ldc, out);
+#pragma unroll
+      for (int q = 0; q < V; q++)
+        out[q] = convert<T, A>(ReduceOp<R>::f(A(ACC ? out[q] : ident), quo[q]));
+      st_stream_32B(cp + i * ldc, out);
+    }
+  } else {
 #pragma unroll 4
   for (int64_t i = r0; i < r1; i++) {
     const T av = __ldg(a + i * lda);
@@ -101,6 +139,7 @@ __global__ void __launch_bounds__(256) outer_vec_kernel(T* __restrict__ c, const
       for (int q = 0; q < V; q++) out[q] = outer_elem<T, C, R>(av, bv[q], ident);
     }
     st_stream_32B(cp + i * ldc, out);
+  }
   }
 }
 

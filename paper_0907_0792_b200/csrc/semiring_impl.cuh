@@ -25,9 +25,11 @@
 // Shared-memory layout: both tiles are stored as k-PAIRS, As[kp][m] =
 // (A[m][2kp], A[m][2kp+1]) and Bs[kp][n] = (B[2kp][n], B[2kp+1][n]), so a
 // thread's FADD2 operands are single 64-bit LDS results.  Thread (ty, tx) owns
-// rows ty*TM..ty*TM+TM-1 and columns 32g + 2tx + {0,1} (g < TN/2): A reads are
-// warp-broadcasts, B reads are 16-byte loads over a contiguous 256-byte span
-// (conflict-free).  Global->shared staging is element-wise cp.async (3 stages).
+// rows ty*TM..ty*TM+TM-1; in the packed fast loop columns 32g + 2tx + {0,1}
+// (g < TN/2, 16-byte loads of two column pairs), in the exact loop columns
+// 16j + tx (one element load per column and k).  A reads are warp-broadcasts
+// and a warp's B reads cover one contiguous span either way.
+// Global->shared staging is element-wise cp.async (3 stages).
 #pragma once
 
 #include <type_traits>
@@ -133,6 +135,13 @@ __global__ void __launch_bounds__(SNT, MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KPair<T>* As = reinterpret_cast<KPair<T>*>(smem_raw);
   KPair<T>* Bs = As + STAGES * Shape::A_STAGE;
+  // division: RN(1/b) (float64) of the current B stage, [BK][BN]; for
+  // float64 NaN where b is outside the reciprocal path's range (so every
+  // proof using it fails), for int64 the reciprocal of double(b).  (int32
+  // keeps the native division: the f64 conversions cost more than they save,
+  // profiles/r01_route_sweep_4096.jsonl.)
+  constexpr bool RCP = C == C_DIV && sizeof(A) == 8;
+  double* Ys = reinterpret_cast<double*>(Bs + STAGES * Shape::B_STAGE);
 
   // grouped rasterisation: GROUP_M row tiles sweep the column tiles together
   const int64_t pid = blockIdx.x;
@@ -144,15 +153,22 @@ __global__ void __launch_bounds__(SNT, MINB)
 
   const int tid = threadIdx.x;
   const int ty = tid >> 4, tx = tid & 15;
+  // The packed fast loop reads column PAIRS (32g + 2tx + {0,1}, one 16-byte
+  // load per two columns); the exact loop reads single elements, so its thread
+  // owns columns 16j + tx and a warp's 16 loads per j hit one contiguous run
+  // of k-pairs (the old 32g + 2tx mapping put them 2 pairs apart: 4-way bank
+  // conflicts for double, 2-way for float).
+  constexpr bool PACKED = MODEK >= 1 && sizeof(T) == 4;
+  auto col_of = [&](int j) { return PACKED ? 32 * (j >> 1) + 2 * tx + (j & 1) : 16 * j + tx; };
 
-  // ---- accumulators: rows ty*TM+i, columns 32*(j>>1) + 2*tx + (j&1) ----
+  // ---- accumulators: rows ty*TM+i, columns col_of(j) ----
   A acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; i++)
 #pragma unroll
     for (int j = 0; j < TN; j++) {
       const int64_t row = m0 + ty * TM + i;
-      const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
+      const int64_t col = n0 + col_of(j);
       if (ACC && row < M && col < N)
         acc[i][j] = A(c[row * ldc + col]);
       else
@@ -222,8 +238,20 @@ __global__ void __launch_bounds__(SNT, MINB)
     const KPair<T>* bs = Bs + (int)(kt % STAGES) * Shape::B_STAGE;
     const int64_t krem = K - kt * BK;
     const int kend = krem < BK ? (int)krem : BK;
+    if constexpr (RCP) {
+      // the previous stage's readers passed the barrier above, so Ys is free
+#pragma unroll
+      for (int q = 0; q < BK * BN / SNT; q++) {
+        const int e = tid + q * SNT, k = e / BN, n = e % BN;
+        const double bval = double(reinterpret_cast<const T*>(bs + (k >> 1) * BN + n)[k & 1]);
+        Ys[k * BN + n] = (std::is_integral<A>::value || rcp_range(bval))
+                             ? rcp_rn(bval)
+                             : __longlong_as_double(0x7ff8000000000000ll);
+      }
+      __syncthreads();
+    }
 
-    if constexpr (MODEK >= 1 && sizeof(T) == 4) {
+    if constexpr (PACKED) {
       constexpr bool INTFOLD = MODEK == 2;
       auto fast_pair = [&](int kp) {
         KPair<float> ap[TM], bp[TN];
@@ -269,20 +297,55 @@ __global__ void __launch_bounds__(SNT, MINB)
         }
       }
     } else {
-      // exact loop: the reference's fold, k ascending, k beyond K skipped
+      // exact loop: the reference's fold, k ascending, k beyond K skipped.
+      // A elements are warp-broadcast loads; the B elements of columns
+      // 16j + tx sit one k-pair apart, so a warp's 16 loads per j span 128
+      // (float) or 256 (double) contiguous bytes.
       for (int kk = 0; kk < kend; kk++) {
         const T* ak = reinterpret_cast<const T*>(as + (kk >> 1) * BM + ty * TM) + (kk & 1);
-        const T* bk = reinterpret_cast<const T*>(bs + (kk >> 1) * BN + 2 * tx) + (kk & 1);
+        const T* bk = reinterpret_cast<const T*>(bs + (kk >> 1) * BN + tx) + (kk & 1);
         A av[TM], bv[TN];
 #pragma unroll
         for (int i = 0; i < TM; i++) av[i] = A(ak[2 * i]);
 #pragma unroll
-        for (int j = 0; j < TN; j++) bv[j] = A(bk[2 * (32 * (j >> 1) + (j & 1))]);
+        for (int j = 0; j < TN; j++) bv[j] = A(bk[2 * 16 * j]);
+        if constexpr (RCP && std::is_integral<A>::value) {
+          double yv[TN];
 #pragma unroll
-        for (int i = 0; i < TM; i++)
+          for (int j = 0; j < TN; j++) yv[j] = Ys[kk * BN + 16 * j + tx];
 #pragma unroll
-          for (int j = 0; j < TN; j++)
-            acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
+          for (int i = 0; i < TM; i++) {
+            const double xd = double(av[i]);
+#pragma unroll
+            for (int j = 0; j < TN; j++)
+              acc[i][j] = ReduceOp<R>::f(acc[i][j], idiv_by_rcp(av[i], xd, bv[j], yv[j]));
+          }
+        } else if constexpr (RCP) {
+          // each row's TN quotients from the staged reciprocals, proven
+          // together (div_candidate); a failed proof redoes the row exactly
+          double yv[TN];
+#pragma unroll
+          for (int j = 0; j < TN; j++) yv[j] = Ys[kk * BN + 16 * j + tx];
+#pragma unroll
+          for (int i = 0; i < TM; i++) {
+            A q[TN];
+            bool ok = rcp_range(av[i]);
+#pragma unroll
+            for (int j = 0; j < TN; j++) q[j] = div_candidate(av[i], bv[j], yv[j], ok);
+            if (!ok) {
+#pragma unroll
+              for (int j = 0; j < TN; j++) q[j] = CombineOp<C_DIV>::f(av[i], bv[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < TN; j++) acc[i][j] = ReduceOp<R>::f(acc[i][j], q[j]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < TN; j++)
+              acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
+        }
       }
     }
   }
@@ -295,7 +358,7 @@ __global__ void __launch_bounds__(SNT, MINB)
     if (row >= M) continue;
 #pragma unroll
     for (int j = 0; j < TN; j++) {
-      const int64_t col = n0 + 32 * (j >> 1) + 2 * tx + (j & 1);
+      const int64_t col = n0 + col_of(j);
       if (col < N) c[row * ldc + col] = convert<T, A>(acc[i][j]);
     }
   }
@@ -341,7 +404,9 @@ template <typename T, int C, int R, bool ACC, int MODEK, int TM = DefaultTile<T,
 cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
   using Shape = SemiringShape<T, R, TM, TN, MINB>;
   auto kern = semiring_kernel<T, C, R, ACC, MODEK, TM, TN, MINB>;
-  const size_t smem = Shape::SMEM;
+  using Acc = typename AccType<T, R>::type;
+  constexpr bool RCP = C == C_DIV && sizeof(Acc) == 8;
+  const size_t smem = Shape::SMEM + (RCP ? (size_t)Shape::BK * Shape::BN * sizeof(double) : 0);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + Shape::BM - 1) / Shape::BM;

@@ -398,6 +398,100 @@ def test_tropical_tma_strided_rows_odd_k(rng):
             assert not np.delete(got, np.s_[0::step], axis=0).any()
 
 
+def _division_operands(rng, n, dt):
+    """n dividends and n divisors spanning every exponent, mantissas of all
+    ones, powers of two, the reciprocal path's range edges, zeros,
+    subnormals, infinities and NaN (div_by_rcp in moa_common.cuh)."""
+    if dt == np.float64:
+        bits = rng.integers(0, 2**63, size=n, dtype=np.uint64) | \
+            (rng.integers(0, 2, size=n, dtype=np.uint64) << np.uint64(63))
+        x = bits.view(np.float64).copy()
+        edges = [2.0**400, 2.0**-400, np.nextafter(2.0**400, 0), np.nextafter(2.0**-400, 0),
+                 2.0 - 2.0**-52, 1.0 - 2.0**-53, 1.5, 3.0, 2.0**-1074, 2.0**-1022, 1.7976931348623157e308]
+    else:
+        bits = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+        x = bits.view(np.float32).copy()
+        edges = [2.0**40, 2.0**-40, float(np.nextafter(np.float32(2.0**40), np.float32(0))),
+                 float(np.nextafter(np.float32(2.0**-40), np.float32(0))), 2.0 - 2.0**-23,
+                 1.0 - 2.0**-24, 1.5, 3.0, 2.0**-149, 2.0**-126, 3.4028234663852886e38]
+    k = n // 4
+    x[:k] = (rng.random(k) * 2 - 1) * 10.0 ** rng.integers(-5, 6, size=k)  # everyday values
+    e = np.array(edges + [-v for v in edges] + [0.0, -0.0, np.inf, -np.inf, np.nan], dtype=dt)
+    x[k:k + e.size] = e
+    x[k + e.size:k + e.size + 64] = 2.0 ** rng.integers(-60, 60, size=64)  # powers of two
+    return rng.permutation(x)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_division_by_reciprocal_is_correctly_rounded(dt, rng):
+    """Every quotient the exact loop forms with div_by_rcp equals RN(a/b): K=2
+    folds whose second term cannot change the first (a zero added, an
+    infinity that loses the min/max), so each result element is one quotient."""
+    n = 1024
+    a_col, b_row = _division_operands(rng, n, dt), _division_operands(rng, n, dt)
+    for red, filler in (("add", 0.0), ("min", np.inf), ("max", -np.inf)):
+        ops = op_pair("divide", red)
+        c, r = ops.codes()
+        a = np.empty((n, 2), dtype=dt)
+        a[:, 0], a[:, 1] = a_col, filler
+        b = np.empty((2, n), dtype=dt)
+        b[0], b[1] = b_row, 1.0
+        want = oracle.product(a.ravel(), b.ravel(), n, 2, n, c, r)
+        got = moa.inner(MoaArray((n, 2), a.ravel(), dtype=dt), MoaArray((2, n), b.ravel(), dtype=dt),
+                        ops).data
+        assert_bits_equal(got, want.astype(dt), f"{np.dtype(dt).name} divide/{red}")
+        if red == "add":  # the quotients themselves, against numpy's IEEE division
+            with np.errstate(all="ignore"):
+                q = (a_col[:, None].astype(np.float64) / b_row[None, :].astype(np.float64))
+            ref = ((0.0 + q) + 0.0).astype(dt).ravel()
+            assert_bits_equal(got, ref, f"{np.dtype(dt).name} quotients")
+            # the outer product's streaming kernel (one reciprocal per column)
+            out = moa.outer(MoaArray((n,), a_col, dtype=dt), MoaArray((n,), b_row, dtype=dt),
+                            ops).data
+            assert_bits_equal(out, (0.0 + q).astype(dt).ravel(), f"{np.dtype(dt).name} outer")
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+def test_integer_division_by_reciprocal_exact(dt, rng):
+    """Integer quotients through the float64 reciprocal (idiv_by_rcp) equal
+    truncating division for full-range operands and the edges: 0, +-1, MIN,
+    MAX, powers of two, exact multiples (where the estimate falls one short)."""
+    info = np.iinfo(dt)
+    n = 1024
+
+    def operands():
+        x = rng.integers(info.min, info.max, size=n, endpoint=True, dtype=np.int64).astype(dt)
+        k = n // 4
+        x[:k] = rng.integers(-1000, 1000, size=k)
+        edges = [0, 1, -1, 2, -2, 3, info.min, info.max, info.min + 1, info.max - 1,
+                 info.max // 2, info.min // 2, 7, -7, 1 << 20, -(1 << 20)]
+        x[k:k + len(edges)] = edges
+        p2 = rng.integers(0, info.bits - 1, size=64)
+        x[k + len(edges):k + len(edges) + 64] = [(1 << int(e)) * (1 if i % 2 else -1)
+                                                 for i, e in enumerate(p2)]
+        return rng.permutation(x)
+
+    xs, ys = operands(), operands()
+    # exact multiples: dividends q*y for random (q, y) pairs
+    ys[:128] = rng.integers(-50000, 50000, size=128)
+    xs[:128] = ys[:128].astype(object) * rng.integers(-40000, 40000, size=128)
+    a = np.empty((n, 2), dtype=dt)
+    a[:, 0], a[:, 1] = xs, 0
+    b = np.empty((2, n), dtype=dt)
+    b[0], b[1] = ys, 1
+    got = moa.inner(MoaArray((n, 2), a.ravel(), dtype=dt), MoaArray((2, n), b.ravel(), dtype=dt),
+                    op_pair("divide", "add")).data.reshape(n, n)
+    xo, yo = xs.astype(object)[:, None], ys.astype(object)[None, :]
+    mag = np.vectorize(lambda x, y: 0 if y == 0 else (abs(x) // abs(y)) * (1 if (x < 0) == (y < 0) else -1),
+                       otypes=[object])(xo, yo)
+    span = 1 << info.bits
+    want = ((mag - info.min) % span + info.min).astype(dt)  # MIN / -1 wraps to MIN
+    np.testing.assert_array_equal(got, want)
+    out = moa.outer(MoaArray((n,), xs, dtype=dt), MoaArray((n,), ys, dtype=dt),
+                    op_pair("divide", "add")).data.reshape(n, n)
+    np.testing.assert_array_equal(out, want)
+
+
 def test_launch_counter_advances():
     from paper_0907_0792_b200 import _native
     before = _native.launch_count()

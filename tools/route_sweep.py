@@ -42,16 +42,22 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--out", default="gpurun_out/route_sweep.jsonl")
+    ap.add_argument("--only", default=None, help="dtype:combine:reduce, e.g. float64:add:min")
     args = ap.parse_args()
     n = args.n
     gen = np.random.default_rng(0)
     plan = plan_inner((n, n), (n, n))
     lines = []
+    only = args.only.split(":") if args.only else None
     for dt in (np.float64, np.float32, np.int32, np.int64):
+        if only and np.dtype(dt).name != only[0]:
+            continue
         a, b = operands(dt, n, gen)
         res = torch.empty(n * n, dtype=a.dtype, device="cuda")
         for comb in moa.COMBINE_OPS:
             for red in moa.REDUCE_OPS:
+                if only and (comb, red) != (only[1], only[2]):
+                    continue
                 ops = moa.op_pair(comb, red)
                 c, r = ops.codes()
                 kern = _native.plan_kernel(native_dtype(np.dtype(dt)), n, n, n, c, r, 0)
