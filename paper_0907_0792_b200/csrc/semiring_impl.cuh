@@ -339,6 +339,19 @@ __global__ void __launch_bounds__(SNT, MINB)
 #pragma unroll
             for (int j = 0; j < TN; j++) acc[i][j] = ReduceOp<R>::f(acc[i][j], q[j]);
           }
+        } else if constexpr (std::is_same<A, int32_t>::value && (C == C_ADD || C == C_SUB) &&
+                             (R == R_MIN || R == R_MAX)) {
+          // int32 tropical: one DPX add-then-min/max (VIADDMNMX) per pair;
+          // the add wraps like wrap_add and subtract adds the wrapped negation
+#pragma unroll
+          for (int j = 0; j < TN; j++)
+            if (C == C_SUB) bv[j] = wrap_sub(int32_t(0), bv[j]);
+#pragma unroll
+          for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < TN; j++)
+              acc[i][j] = R == R_MIN ? __viaddmin_s32(av[i], bv[j], acc[i][j])
+                                     : __viaddmax_s32(av[i], bv[j], acc[i][j]);
         } else {
 #pragma unroll
           for (int i = 0; i < TM; i++)

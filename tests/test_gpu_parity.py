@@ -581,6 +581,26 @@ def test_integer_large_random_matches_int_reference(rng):
         np.testing.assert_array_equal(mn.data.reshape(m, n), want)
 
 
+def test_integer_tropical_wraps(rng):
+    """int32/int64 (add|subtract, min|max) over full-range values: the sums
+    wrap (two's complement) before the fold, as in the exact loop's wrap_add;
+    int32 runs on the DPX add-then-min/max instruction (VIADDMNMX)."""
+    for dt in (np.int32, np.int64):
+        info = np.iinfo(dt)
+        m, k, n = 70, 45, 130
+        a = rng.integers(info.min, info.max, size=(m, k), endpoint=True, dtype=np.int64).astype(dt)
+        b = rng.integers(info.min, info.max, size=(k, n), endpoint=True, dtype=np.int64).astype(dt)
+        a[0, :4] = [info.max, info.min, 0, -1]
+        b[:4, 0] = [info.max, info.min, 1, info.min]
+        for comb, red in (("add", "min"), ("add", "max"), ("subtract", "min"), ("subtract", "max")):
+            with np.errstate(over="ignore"):
+                s3 = (a[:, :, None] + b[None, :, :]) if comb == "add" else (a[:, :, None] - b[None, :, :])
+            want = s3.min(axis=1) if red == "min" else s3.max(axis=1)
+            got = moa.inner(MoaArray((m, k), a.ravel(), dtype=dt), MoaArray((k, n), b.ravel(), dtype=dt),
+                            op_pair(comb, red)).data.reshape(m, n)
+            np.testing.assert_array_equal(got, want, err_msg=f"{np.dtype(dt).name} {comb}/{red}")
+
+
 def test_k_chunked_accumulation_replays_one_pass(rng):
     """Accumulating k-chunks (slab-aligned) with MOA_FLAG_ACCUMULATE gives the
     bits of one DMMA pass — what the pipelined broadcast of B relies on."""
