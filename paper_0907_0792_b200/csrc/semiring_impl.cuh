@@ -13,22 +13,20 @@
 //
 // For combine in {add, subtract} with reduce in {min, max} on float32 — the
 // tropical semirings, BASELINE config 5 — the exact loop costs a FADD, FSETP
-// and FSEL per pair.  The fast loops add two contraction steps at once with a
-// packed FADD2 and fold both sums with one 3-input min/max: VIMNMX3 on the bit
-// patterns when every combine result is a non-negative float, FMNMX3 when no
-// combine result can be NaN or -0.0 (moa_common.cuh).  A pre-scan kernel
-// records which special values occur in A and B; the host launches one kernel
-// specialisation per fold mode and all but the one the device flags select
+// and FSEL per pair; the fast loops of tropical.cuh add two contraction steps
+// at once with a packed FADD2 and fold both sums with one 3-input min/max
+// (VIMNMX3 on the bit patterns when every combine result is a non-negative
+// float, FMNMX3 when no combine result can be NaN or -0.0, moa_common.cuh).
+// A pre-scan kernel here records which special values occur in A and B; the
+// host launches one kernel per fold mode (this file's MODEK = 0 exact
+// specialisation among them) and all but the one the device flags select
 // return at once, so there is no host synchronisation and the result never
 // depends on the choice.
 //
 // Shared-memory layout: both tiles are stored as k-PAIRS, As[kp][m] =
-// (A[m][2kp], A[m][2kp+1]) and Bs[kp][n] = (B[2kp][n], B[2kp+1][n]), so a
-// thread's FADD2 operands are single 64-bit LDS results.  Thread (ty, tx) owns
-// rows ty*TM..ty*TM+TM-1; in the packed fast loop columns 32g + 2tx + {0,1}
-// (g < TN/2, 16-byte loads of two column pairs), in the exact loop columns
-// 16j + tx (one element load per column and k).  A reads are warp-broadcasts
-// and a warp's B reads cover one contiguous span either way.
+// (A[m][2kp], A[m][2kp+1]) and Bs[kp][n] = (B[2kp][n], B[2kp+1][n]).  Thread
+// (ty, tx) owns rows ty*TM..ty*TM+TM-1 and columns 16j + tx; A reads are
+// warp-broadcasts and a warp's B reads per j cover one contiguous span.
 // Global->shared staging is element-wise cp.async (3 stages).
 #pragma once
 
@@ -86,22 +84,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__device__ __forceinline__ unsigned long long f32x2_bits(KPair<float> p) {
-  return *reinterpret_cast<unsigned long long*>(&p);
-}
-
-// one FADD2: (a.x op b.x, a.y op b.y), round-to-nearest each
-template <int C>
-__device__ __forceinline__ void pair_combine(KPair<float> a, KPair<float> b, float& s0, float& s1) {
-  unsigned long long r;
-  if (C == C_SUB)
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f32x2_bits(a)), "l"(f32x2_bits(b)));
-  else
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f32x2_bits(a)), "l"(f32x2_bits(b)));
-  s0 = __uint_as_float((unsigned)r);
-  s1 = __uint_as_float((unsigned)(r >> 32));
-}
-
+// 3-input fold of the tropical fast loops (tropical.cuh)
 template <int R, bool INTFOLD>
 __device__ __forceinline__ float fold3(float acc, float s0, float s1) {
   if (INTFOLD) {  // non-negative floats: unsigned order == float order
@@ -116,10 +99,9 @@ __device__ __forceinline__ float fold3(float acc, float s0, float s1) {
   return r;
 }
 
-// MODEK: -1 = exact fold only (no pre-scan); 0 / 1 / 2 = the exact / FMNMX3 /
-// VIMNMX3 specialisation of a tropical candidate, which returns at once unless
-// the device-side pre-scan selected that mode (one loop per kernel keeps
-// register pressure down).
+// MODEK: -1 = exact fold only (no pre-scan); 0 = the exact specialisation of a
+// tropical candidate, which returns at once unless the device-side pre-scan
+// selected the exact loop (modes 1 and 2 are the kernels of tropical.cuh).
 template <typename T, int C, int R, bool ACC, int MODEK, int TM, int TN, int MINB>
 __global__ void __launch_bounds__(SNT, MINB)
     semiring_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ b,
@@ -153,13 +135,10 @@ __global__ void __launch_bounds__(SNT, MINB)
 
   const int tid = threadIdx.x;
   const int ty = tid >> 4, tx = tid & 15;
-  // The packed fast loop reads column PAIRS (32g + 2tx + {0,1}, one 16-byte
-  // load per two columns); the exact loop reads single elements, so its thread
-  // owns columns 16j + tx and a warp's 16 loads per j hit one contiguous run
-  // of k-pairs (the old 32g + 2tx mapping put them 2 pairs apart: 4-way bank
-  // conflicts for double, 2-way for float).
-  constexpr bool PACKED = MODEK >= 1 && sizeof(T) == 4;
-  auto col_of = [&](int j) { return PACKED ? 32 * (j >> 1) + 2 * tx + (j & 1) : 16 * j + tx; };
+  // Thread (ty, tx) owns columns 16j + tx: a warp's 16 B loads per j hit one
+  // contiguous run of k-pairs (a 32g + 2tx mapping puts them 2 pairs apart:
+  // 4-way bank conflicts for double, 2-way for float).
+  auto col_of = [&](int j) { return 16 * j + tx; };
 
   // ---- accumulators: rows ty*TM+i, columns col_of(j) ----
   A acc[TM][TN];
@@ -174,16 +153,6 @@ __global__ void __launch_bounds__(SNT, MINB)
       else
         acc[i][j] = ReduceOp<R>::template identity<A>();
     }
-  // The unsigned-order fold (mode 2) cannot start from -inf (sign bit set).
-  // Mode 2 implies every combine result is >= +0 and K >= 2, so a max fold
-  // from +0 gives the same bits as one from the identity.
-  if constexpr (R == R_MAX && MODEK == 2) {
-#pragma unroll
-    for (int i = 0; i < TM; i++)
-#pragma unroll
-      for (int j = 0; j < TN; j++) acc[i][j] = A(0);
-  }
-
   // ---- element-wise async copies into the k-pair layouts (zero-filled outside) ----
   // Per-thread bases are fixed for the whole kernel; a stage only adds k0.
   const int a_kk = tid % BK, a_r = tid / BK;
@@ -251,52 +220,7 @@ __global__ void __launch_bounds__(SNT, MINB)
       __syncthreads();
     }
 
-    if constexpr (PACKED) {
-      constexpr bool INTFOLD = MODEK == 2;
-      auto fast_pair = [&](int kp) {
-        KPair<float> ap[TM], bp[TN];
-        const float4* pa4 = reinterpret_cast<const float4*>(as + kp * BM + ty * TM);
-#pragma unroll
-        for (int q = 0; q < TM / 2; q++) {
-          const float4 v = pa4[q];
-          ap[2 * q] = KPair<float>{v.x, v.y};
-          ap[2 * q + 1] = KPair<float>{v.z, v.w};
-        }
-#pragma unroll
-        for (int g = 0; g < TN / 2; g++) {
-          const float4 v = *reinterpret_cast<const float4*>(bs + kp * BN + 32 * g + 2 * tx);
-          bp[2 * g] = KPair<float>{v.x, v.y};
-          bp[2 * g + 1] = KPair<float>{v.z, v.w};
-        }
-#pragma unroll
-        for (int i = 0; i < TM; i++)
-#pragma unroll
-          for (int j = 0; j < TN; j++) {
-            float s0, s1;
-            pair_combine<C>(ap[i], bp[j], s0, s1);
-            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], s0, s1);
-          }
-      };
-      if (kend == BK) {
-#pragma unroll
-        for (int kp = 0; kp < KP; kp++) fast_pair(kp);
-      } else {
-        for (int kp = 0; kp < kend / 2; kp++) fast_pair(kp);
-        if (kend & 1) {  // lone last k: one scalar combine + 2-input min/max
-          const int kp = kend / 2;
-          float av[TM], bv[TN];
-#pragma unroll
-          for (int i = 0; i < TM; i++) av[i] = as[kp * BM + ty * TM + i].x;
-#pragma unroll
-          for (int j = 0; j < TN; j++) bv[j] = bs[kp * BN + 32 * (j >> 1) + 2 * tx + (j & 1)].x;
-#pragma unroll
-          for (int i = 0; i < TM; i++)
-#pragma unroll
-            for (int j = 0; j < TN; j++)
-              acc[i][j] = ReduceOp<R>::f(acc[i][j], CombineOp<C>::f(av[i], bv[j]));
-        }
-      }
-    } else {
+    {
       // exact loop: the reference's fold, k ascending, k beyond K skipped.
       // A elements are warp-broadcast loads; the B elements of columns
       // 16j + tx sit one k-pair apart, so a warp's 16 loads per j span 128

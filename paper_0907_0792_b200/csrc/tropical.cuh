@@ -1,10 +1,12 @@
 // K2 fast loops for the float32 tropical semirings — combine in {add, subtract},
 // reduce in {min, max} (BASELINE config 5) — in their own kernel.
 //
-// Operands stay in their natural row-major layouts in shared memory
-// (A[BM][BK+4], B[BK][BN+4]) so both tiles are filled with 16-byte cp.async
-// chunks.  A thread owns rows ty*8+i and columns 64g + 4tx + c (g < 2, c < 4)
-// of a 128x128 C tile.  For each k-pair (k, k+1) it forms, per row i and
+// Two kernels share the loop: tropical_tma_kernel (16-byte aligned rows:
+// TMA-staged tiles, mbarrier pipeline, no block barrier in the main loop) and
+// tropical_kernel (any alignment: cp.async into padded A[BM][BK+4],
+// B[BK][BN+4]).  Operands stay in their natural row-major layouts; a thread
+// owns 8 rows and columns 64g + 4tx + c (g < 2, c < 4) of a 128x128 C tile.
+// For each k-pair (k, k+1) it forms, per row i and
 // column pair (j, j+1),
 //     s  = FADD2((B[k][j],   B[k][j+1]),   a[i][k]   broadcast)
 //     s' = FADD2((B[k+1][j], B[k+1][j+1]), a[i][k+1] broadcast)
@@ -55,9 +57,7 @@ __device__ __forceinline__ float hi32(unsigned long long v) {
   return __uint_as_float((unsigned)(v >> 32));
 }
 
-// QUAD: fetch A as 16-byte rows covering two k-pairs (8 shared loads per
-// k-pair instead of 12) at the cost of keeping four B rows live.
-template <int C, int R, int MODE, bool VEC, bool QUAD>
+template <int C, int R, int MODE, bool VEC>
 __global__ void __launch_bounds__(TNT, 2)
     tropical_kernel(float* __restrict__ c, const float* __restrict__ a, const float* __restrict__ b,
                     int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
@@ -173,43 +173,8 @@ __global__ void __launch_bounds__(TNT, 2)
       }
     };
     const int npairs = kend >> 1;
-    int kp0 = 0;
-    if constexpr (QUAD) {
-      // two k-pairs per step: B rows k..k+3, A as one 16-byte load per row
 #pragma unroll 1
-      for (; kp0 + 2 <= npairs; kp0 += 2) {
-        const int k = 2 * kp0;
-        float4 bq[4][2];
-#pragma unroll
-        for (int r = 0; r < 4; r++)
-#pragma unroll
-          for (int g = 0; g < 2; g++)
-            bq[r][g] = *reinterpret_cast<const float4*>(bs + (k + r) * TLDB + 64 * g);
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-          const float4 av = *reinterpret_cast<const float4*>(as + i * TLDA + k);
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const float a0 = h ? av.z : av.x, a1 = h ? av.w : av.y;
-#pragma unroll
-            for (int g = 0; g < 2; g++)
-#pragma unroll
-              for (int p = 0; p < 2; p++) {
-                const float4 r0 = bq[2 * h][g], r1 = bq[2 * h + 1][g];
-                const unsigned long long s =
-                    pair_op_bcast<C>(p ? r0.z : r0.x, p ? r0.w : r0.y, a0);
-                const unsigned long long t =
-                    pair_op_bcast<C>(p ? r1.z : r1.x, p ? r1.w : r1.y, a1);
-                const int j = 4 * g + 2 * p;
-                acc[i][j] = fold3<R, INTFOLD>(acc[i][j], lo32(s), lo32(t));
-                acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], hi32(s), hi32(t));
-              }
-          }
-        }
-      }
-    }
-#pragma unroll 1
-    for (int kp = kp0; kp < npairs; kp++) kpair(2 * kp);
+    for (int kp = 0; kp < npairs; kp++) kpair(2 * kp);
     {
       const int k4 = 2 * npairs;
       if (k4 < kend) {  // lone last k: scalar combine + 2-input fold
@@ -423,19 +388,15 @@ cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
   return cudaGetLastError();
 }
 
-#ifndef MOA_TROPICAL_QUAD
-#define MOA_TROPICAL_QUAD false
-#endif
-
-template <int C, int R, int MODE, bool QUAD = MOA_TROPICAL_QUAD>
+template <int C, int R, int MODE>
 cudaError_t tropical_launch(const Problem& p, const unsigned* special) {
   // TMA-staged kernel when the layout allows it: 19.5 vs 18.6 T pairs/s at c5
   // (profiles/r01_tune_tropical_tma.jsonl); bit-identical results
-  if (!QUAD && tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE>(p, special);
+  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE>(p, special);
   const bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
-  auto kern = vec ? tropical_kernel<C, R, MODE, true, QUAD> : tropical_kernel<C, R, MODE, false, QUAD>;
+  auto kern = vec ? tropical_kernel<C, R, MODE, true> : tropical_kernel<C, R, MODE, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
