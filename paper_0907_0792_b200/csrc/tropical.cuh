@@ -228,8 +228,8 @@ constexpr int TT_A_BYTES = TBM * TBK * 4, TT_B_BYTES = TBK * TBN * 4;  // 16 KiB
 constexpr int TT_STAGE_BYTES = TT_A_BYTES + TT_B_BYTES;
 constexpr size_t TT_SMEM = (size_t)TSTAGES * TT_STAGE_BYTES + 1024 + 64;
 
-template <int C, int R, int MODE>
-__global__ void __launch_bounds__(TNT, 2)
+template <int C, int R, int MODE, int MINB = 2, int UNR = 1>
+__global__ void __launch_bounds__(TNT, MINB)
     tropical_tma_kernel(float* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                         const unsigned* special, int64_t tiles_m, int64_t tiles_n,
                         const __grid_constant__ CUtensorMap map_a,
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(TNT, 2)
     const int64_t krem = K - kt * TBK;
     const int kend = krem < TBK ? (int)krem : TBK;
     const int npairs = kend >> 1;
-#pragma unroll 1
+#pragma unroll UNR
     for (int kp = 0; kp < npairs; kp++) {
       const int k = 2 * kp;
       const int aoff = ((((k >> 2) ^ ty) & 7) << 4) + ((k & 3) << 2);
@@ -370,13 +370,13 @@ inline bool tropical_tma_eligible(const Problem& p) {
          p.ldb < (int64_t(1) << 36) && tensor_maps_available();
 }
 
-template <int C, int R, int MODE>
+template <int C, int R, int MODE, int MINB = 2, int UNR = 1>
 cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
   CUtensorMap map_a, map_b;
   if (!make_tensor_map_2d(&map_a, p.a, 4, p.M, p.K, p.lda, TBM, TBK, true) ||
       !make_tensor_map_2d(&map_b, p.b, 4, p.K, p.N, p.ldb, TBK, TBN, false))
     return cudaErrorInvalidValue;
-  auto kern = tropical_tma_kernel<C, R, MODE>;
+  auto kern = tropical_tma_kernel<C, R, MODE, MINB, UNR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT_SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
