@@ -375,6 +375,33 @@ def test_tropical_fast_and_exact_loops_agree(mkn, rng):
                 assert_bits_equal(got, want, f"{ops} poison={poison}")
 
 
+@pytest.mark.parametrize("mkn", [(20000, 48, 8), (12000, 4, 4), (9600, 132, 16), (12000, 2, 2)])
+def test_tma_kernels_on_skinny_shapes(mkn, rng):
+    """Boxes wider than the matrix (N below the 16/128-column TMA box, K below
+    the 16/32-deep slab): the out-of-bounds fill must not leak into results.
+    (x,+) float64 against the cp.async kernel on a row subset (bitwise) and the
+    reference (tolerance); (add,min) float32 bitwise against the reference."""
+    torch = _torch()
+    m, k, n = mkn
+    a = rng.random(m * k) * 2 - 1
+    b = rng.random(k * n) * 2 - 1
+    ad, bd = _dev(a), _dev(b)
+    full = torch.empty(m * n, dtype=torch.float64, device="cuda")
+    launch(plan_inner((m, k), (k, n)), full, ad, bd, moa.MUL_ADD)
+    sub = torch.empty(64 * n, dtype=torch.float64, device="cuda")
+    launch(plan_inner((64, k), (k, n)), sub, ad[:64 * k], bd, moa.MUL_ADD)
+    full = full.cpu().numpy()
+    assert_bits_equal(sub.cpu().numpy(), full[:64 * n])
+    assert_within(full, oracle.product(a, b, m, k, n, MUL, ADD), sum_tolerance(k, a, b))
+    if k % 4 == 0 and n % 4 == 0:  # 16-byte rows: the TMA tropical kernel
+        a32 = (rng.random(m * k) * 100).astype(np.float32)
+        b32 = (rng.random(k * n) * 100).astype(np.float32)
+        ops = op_pair("add", "min")
+        got = moa.inner(MoaArray((m, k), a32, dtype=np.float32), MoaArray((k, n), b32, dtype=np.float32),
+                        ops).data
+        assert_bits_equal(got, oracle.product(a32, b32, m, k, n, 0, 2).astype(np.float32))
+
+
 def test_tropical_tma_strided_rows_odd_k(rng):
     """Round-robin row sets (lda = K*step) keep the TMA-staged tropical kernel
     eligible with an odd K, so its lone-k tail runs; bitwise vs the reference."""
