@@ -345,33 +345,36 @@ def test_dmma_tma_edges_bitwise_equal_cp_async_path(rng):
                   sum_tolerance(k, rows, b))
 
 
-@pytest.mark.parametrize("mkn", [(257, 131, 300),   # odd K, unaligned rows: cp.async kernel
-                                 (1000, 132, 1004)])  # 16-byte rows: TMA-staged kernel
-def test_tropical_fast_and_exact_loops_agree(mkn, rng):
-    """float32 (add|subtract, min|max): the VIMNMX3 / FMNMX3 loops (clean data)
-    and the compare-select loop (data with NaN/-0) all equal the reference."""
+@pytest.mark.parametrize("dt,mkn", [(np.float32, (257, 131, 300)),   # odd K, unaligned: cp.async
+                                    (np.float32, (1000, 132, 1004)),  # 16-byte rows: TMA kernel
+                                    (np.float64, (257, 131, 300))])   # exact fold, specials
+def test_tropical_fast_and_exact_loops_agree(dt, mkn, rng):
+    """(add|subtract, min|max): the float32 fast folds (clean data) and the
+    compare-select loop (float64, and data with NaN/-0) all equal the
+    reference.  (A float64 fmin/fmax fold was tried: sm_100a has no DMNMX, it
+    lowers to DSETP + selects and ran 24% slower than compare-select.)"""
     m, k, n = mkn  # odd K: the last k of the last tile takes the scalar tail
     for comb in ("add", "subtract"):
         for red in ("min", "max"):
             ops = op_pair(comb, red)
             c, r = ops.codes()
-            a = rng.random(m * k, dtype=np.float32) * np.float32(100)
-            b = rng.random(k * n, dtype=np.float32) * np.float32(100)
+            a = (rng.random(m * k) * 100).astype(dt)
+            b = (rng.random(k * n) * 100).astype(dt)
             a[rng.random(m * k) < 0.05] = np.inf
             b[rng.random(k * n) < 0.05] = np.inf if comb == "add" else -np.inf
             for poison in (None, "nan", "negzero", "negative"):
                 aa, bb = a.copy(), b.copy()
                 if poison == "negative":  # sign bits set: FMNMX3 loop instead of VIMNMX3
-                    aa = aa - np.float32(50)
+                    aa = aa - dt(50)
                 elif poison == "nan":
                     aa[rng.random(m * k) < 0.01] = np.nan
                 elif poison == "negzero":
                     aa[rng.random(m * k) < 0.05] = -0.0
                     bb[rng.random(k * n) < 0.05] = -0.0 if comb == "add" else 0.0
-                want = oracle.product(aa, bb, m, k, n, c, r).astype(np.float32)
-                got = moa.inner(MoaArray((m, k), aa, dtype=np.float32),
-                                MoaArray((k, n), bb, dtype=np.float32), ops).data
-                assert got.dtype == np.float32
+                want = oracle.product(aa, bb, m, k, n, c, r).astype(dt)
+                got = moa.inner(MoaArray((m, k), aa, dtype=dt),
+                                MoaArray((k, n), bb, dtype=dt), ops).data
+                assert got.dtype == dt
                 assert_bits_equal(got, want, f"{ops} poison={poison}")
 
 
