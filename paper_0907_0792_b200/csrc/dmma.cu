@@ -259,11 +259,13 @@ cudaError_t dmma_launch(const Problem& p) {
 // small: 32x32 CTA, 4 warps of 16x16, BK=32 (few k-tile round trips)
 // tiny: 16x32 CTA, 4 warps of 16x8: the most warps for problems that give
 //       fewer than 148 small tiles (c1: 8.7 vs 10.8 us; one warp already
-//       saturates its sub-partition's DMMA pipe, tools/mb_dmma_latency.cu)
+//       saturates its sub-partition's DMMA pipe, tools/mb_dmma_latency.cu);
+//       8 stages keep a whole 256-deep K in flight (cold-cache ncu: 7.0 vs
+//       8.0 us at c1)
 using CfgLarge = DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>;
 using CfgMedium = DmmaCfg<64, 64, 32, 32, 3, 16, 3>;
 using CfgSmall = DmmaCfg<32, 32, 16, 16, 3, 32, 1>;
-using CfgTiny = DmmaCfg<16, 32, 16, 8, 3, 32, 1>;
+using CfgTiny = DmmaCfg<16, 32, 16, 8, 8, 32, 1>;
 
 template <class Cfg>
 cudaError_t dmma_dispatch(const Problem& p) {
