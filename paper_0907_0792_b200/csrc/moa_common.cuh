@@ -260,4 +260,19 @@ __host__ __device__ inline int tropical_fold_mode(int combine, unsigned fa, unsi
   return 1;
 }
 
+// With MOA_FLAG_ACCUMULATE the result's previous contents are folded too:
+// they must hold no NaN or -0.0 for any fast mode (fc = C's scan flags) and
+// be sign-clear for the unsigned-order fold.
+__host__ __device__ inline int tropical_fold_mode_acc(int combine, unsigned fa, unsigned fb,
+                                                      unsigned fc) {
+  const int m = tropical_fold_mode(combine, fa, fb);
+  if (fc & (S_NAN | S_NZERO)) return 0;
+  return (m == 2 && (fc & S_NEG)) ? 1 : m;
+}
+template <bool ACC>
+__device__ __forceinline__ int tropical_mode_of(int combine, const unsigned* special) {
+  return ACC ? tropical_fold_mode_acc(combine, __ldg(special), __ldg(special + 1), __ldg(special + 2))
+             : tropical_fold_mode(combine, __ldg(special), __ldg(special + 1));
+}
+
 }  // namespace moa

@@ -12,7 +12,8 @@ cudaError_t launch_semiring_i32(const Problem& p);
 cudaError_t launch_semiring_i64(const Problem& p);
 
 bool semiring_fast_candidate(int dtype, int combine, int reduce, bool accumulate) {
-  return dtype == MOA_DTYPE_F32 && !accumulate && (combine == C_ADD || combine == C_SUB) &&
+  (void)accumulate;  // accumulate folds C's contents too; the pre-scan covers them
+  return dtype == MOA_DTYPE_F32 && (combine == C_ADD || combine == C_SUB) &&
          (reduce == R_MIN || reduce == R_MAX);
 }
 

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(SNT, MINB)
   constexpr int STAGES = Shape::STAGES, BM = Shape::BM, BN = Shape::BN;
   constexpr int BK = Shape::BK, KP = Shape::KP;
   if constexpr (MODEK >= 0) {
-    if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODEK) return;
+    if (tropical_mode_of<ACC>(C, special) != MODEK) return;
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KPair<T>* As = reinterpret_cast<KPair<T>*>(smem_raw);
@@ -365,28 +365,36 @@ cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
 namespace moa {
 namespace {
 
+// float32 tropical pair: pre-scan A (M x K, lda), B (K x N, ldb) and, when
+// accumulating, C (M x N, ldc) for NaN / +-inf / +-0 / sign, then launch one
+// specialisation per fold mode; all but the one the flags select exit at once.
+template <int C, int R, bool ACC>
+cudaError_t tropical_candidate(const Problem& p) {
+  unsigned* special = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&special), 3 * sizeof(unsigned), p.stream);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(special, 0, 3 * sizeof(unsigned), p.stream);
+  if (e == cudaSuccess) {
+    launch_scan<float>(static_cast<const float*>(p.a), p.M, p.K, p.lda, special, p.stream);
+    launch_scan<float>(static_cast<const float*>(p.b), p.K, p.N, p.ldb, special + 1, p.stream);
+    if (ACC) launch_scan<float>(static_cast<const float*>(p.c), p.M, p.N, p.ldc, special + 2, p.stream);
+    if constexpr (C == C_ADD) e = tropical_launch<C, R, 2, ACC>(p, special);
+    if (e == cudaSuccess) e = tropical_launch<C, R, 1, ACC>(p, special);
+    if (e == cudaSuccess) e = semiring_launch<float, C, R, ACC, 0>(p, special);
+  }
+  cudaError_t e2 = cudaFreeAsync(special, p.stream);
+  return e != cudaSuccess ? e : e2;
+}
+
 template <typename T, int C, int R>
 cudaError_t semiring_acc(const Problem& p) {
-  if (p.accumulate) return semiring_launch<T, C, R, true, -1>(p, nullptr);
   constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB) &&
                         (R == R_MIN || R == R_MAX);
   if constexpr (cand) {
-    // pre-scan A (M x K, lda) and B (K x N, ldb) for NaN / +-inf / +-0
-    unsigned* special = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&special), 2 * sizeof(unsigned), p.stream);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(special, 0, 2 * sizeof(unsigned), p.stream);
-    if (e != cudaSuccess) return e;
-    launch_scan<T>(static_cast<const T*>(p.a), p.M, p.K, p.lda, special, p.stream);
-    launch_scan<T>(static_cast<const T*>(p.b), p.K, p.N, p.ldb, special + 1, p.stream);
-    // one specialisation per fold mode; all but the selected one exit at once
-    if constexpr (C == C_ADD) e = tropical_launch<C, R, 2>(p, special);
-    if (e == cudaSuccess) e = tropical_launch<C, R, 1>(p, special);
-    if (e == cudaSuccess) e = semiring_launch<T, C, R, false, 0>(p, special);
-    cudaError_t e2 = cudaFreeAsync(special, p.stream);
-    return e != cudaSuccess ? e : e2;
+    return p.accumulate ? tropical_candidate<C, R, true>(p) : tropical_candidate<C, R, false>(p);
   } else {
-    return semiring_launch<T, C, R, false, -1>(p, nullptr);
+    return p.accumulate ? semiring_launch<T, C, R, true, -1>(p, nullptr)
+                        : semiring_launch<T, C, R, false, -1>(p, nullptr);
   }
 }
 

@@ -57,14 +57,37 @@ __device__ __forceinline__ float hi32(unsigned long long v) {
   return __uint_as_float((unsigned)(v >> 32));
 }
 
-template <int C, int R, int MODE, bool VEC>
+// Accumulators of a thread owning rows r0 + rstep*i (i < 8) and columns
+// 64g + 4tx + cc (acc[i][4g + cc]).  From the identity — or, for the
+// unsigned-order max fold, from +0: every combine result is >= +0 there and
+// K >= 1, so the max is unchanged while -inf's sign bit would break the
+// order — or from C's previous contents under MOA_FLAG_ACCUMULATE (whose
+// values the fold mode has already checked).
+template <int R, bool INTFOLD, bool ACC>
+__device__ __forceinline__ void init_acc(float (&acc)[8][8], const float* c, int64_t M, int64_t N,
+                                         int64_t ldc, int64_t m0, int64_t n0, int r0, int rstep,
+                                         int tx) {
+  const float init = (INTFOLD && R == R_MAX) ? 0.0f : ReduceOp<R>::template identity<float>();
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      acc[i][j] = init;
+      if (ACC) {
+        const int64_t row = m0 + r0 + rstep * i, col = n0 + 64 * (j >> 2) + 4 * tx + (j & 3);
+        if (row < M && col < N) acc[i][j] = c[row * ldc + col];
+      }
+    }
+}
+
+template <int C, int R, int MODE, bool ACC, bool VEC>
 __global__ void __launch_bounds__(TNT, 2)
     tropical_kernel(float* __restrict__ c, const float* __restrict__ a, const float* __restrict__ b,
                     int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                     const unsigned* special, int64_t tiles_m, int64_t tiles_n) {
   static_assert(MODE == 1 || MODE == 2, "fast modes only");
   constexpr bool INTFOLD = MODE == 2;
-  if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODE) return;
+  if (tropical_mode_of<ACC>(C, special) != MODE) return;
   extern __shared__ __align__(16) float tsm[];
   float* As = tsm;
   float* Bs = tsm + TSTAGES * TA_STAGE;
@@ -79,12 +102,7 @@ __global__ void __launch_bounds__(TNT, 2)
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
 
   float acc[8][8];
-  const float init = (INTFOLD && R == R_MAX) ? 0.0f  // see semiring_kernel: mode 2 max folds from +0
-                                            : ReduceOp<R>::template identity<float>();
-#pragma unroll
-  for (int i = 0; i < 8; i++)
-#pragma unroll
-    for (int j = 0; j < 8; j++) acc[i][j] = init;
+  init_acc<R, INTFOLD, ACC>(acc, c, M, N, ldc, m0, n0, ty * 8, 1, tx);
 
   // ---- loaders: 16-byte chunks (VEC) or single elements, zero-filled outside ----
   auto load_stage = [&](int stage, int64_t k0) {
@@ -228,7 +246,7 @@ constexpr int TT_A_BYTES = TBM * TBK * 4, TT_B_BYTES = TBK * TBN * 4;  // 16 KiB
 constexpr int TT_STAGE_BYTES = TT_A_BYTES + TT_B_BYTES;
 constexpr size_t TT_SMEM = (size_t)TSTAGES * TT_STAGE_BYTES + 1024 + 64;
 
-template <int C, int R, int MODE, int MINB = 2, int UNR = 1>
+template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1>
 __global__ void __launch_bounds__(TNT, MINB)
     tropical_tma_kernel(float* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                         const unsigned* special, int64_t tiles_m, int64_t tiles_n,
@@ -236,7 +254,7 @@ __global__ void __launch_bounds__(TNT, MINB)
                         const __grid_constant__ CUtensorMap map_b) {
   static_assert(MODE == 1 || MODE == 2, "fast modes only");
   constexpr bool INTFOLD = MODE == 2;
-  if (tropical_fold_mode(C, __ldg(special), __ldg(special + 1)) != MODE) return;
+  if (tropical_mode_of<ACC>(C, special) != MODE) return;
   extern __shared__ __align__(16) unsigned char tt_raw[];
   unsigned char* base = tma::align1k(tt_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + TSTAGES * TT_STAGE_BYTES);
@@ -275,11 +293,7 @@ __global__ void __launch_bounds__(TNT, MINB)
   }
 
   float acc[8][8];
-  const float init = (INTFOLD && R == R_MAX) ? 0.0f : ReduceOp<R>::template identity<float>();
-#pragma unroll
-  for (int i = 0; i < 8; i++)
-#pragma unroll
-    for (int j = 0; j < 8; j++) acc[i][j] = init;
+  init_acc<R, INTFOLD, ACC>(acc, c, M, N, ldc, m0, n0, ty, 16, tx);
 
   for (int64_t kt = 0; kt < KT; kt++) {
     const int stage = (int)(kt % TSTAGES);
@@ -370,13 +384,13 @@ inline bool tropical_tma_eligible(const Problem& p) {
          p.ldb < (int64_t(1) << 36) && tensor_maps_available();
 }
 
-template <int C, int R, int MODE, int MINB = 2, int UNR = 1>
+template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1>
 cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
   CUtensorMap map_a, map_b;
   if (!make_tensor_map_2d(&map_a, p.a, 4, p.M, p.K, p.lda, TBM, TBK, true) ||
       !make_tensor_map_2d(&map_b, p.b, 4, p.K, p.N, p.ldb, TBK, TBN, false))
     return cudaErrorInvalidValue;
-  auto kern = tropical_tma_kernel<C, R, MODE, MINB, UNR>;
+  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT_SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
@@ -388,15 +402,15 @@ cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
   return cudaGetLastError();
 }
 
-template <int C, int R, int MODE>
+template <int C, int R, int MODE, bool ACC>
 cudaError_t tropical_launch(const Problem& p, const unsigned* special) {
   // TMA-staged kernel when the layout allows it: 19.5 vs 18.6 T pairs/s at c5
   // (profiles/r01_tune_tropical_tma.jsonl); bit-identical results
-  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE>(p, special);
+  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE, ACC>(p, special);
   const bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
-  auto kern = vec ? tropical_kernel<C, R, MODE, true> : tropical_kernel<C, R, MODE, false>;
+  auto kern = vec ? tropical_kernel<C, R, MODE, ACC, true> : tropical_kernel<C, R, MODE, ACC, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TSMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;

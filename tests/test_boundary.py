@@ -54,7 +54,8 @@ def test_kernel_routing():
     assert pk(0, 16384, 16384, 16384, 2, 0) == "dmma"
     assert pk(0, 16384, 16384, 16384, 2, 0, _native.FLAG_EXACT) == "semiring_exact"
     assert pk(1, 16384, 16384, 16384, 0, 2) == "semiring_fast"
-    assert pk(1, 16384, 16384, 16384, 0, 2, _native.FLAG_ACCUMULATE) == "semiring_exact"
+    # accumulate folds C's contents too (pre-scanned with A and B)
+    assert pk(1, 16384, 16384, 16384, 0, 2, _native.FLAG_ACCUMULATE) == "semiring_fast"
     assert pk(0, 16384, 16384, 16384, 0, 2) == "semiring_exact"  # no f64 fast loop
     assert pk(1, 16384, 16384, 16384, 2, 0) == "semiring_exact"  # f32 sums run in f64
     assert pk(2, 16384, 16384, 16384, 2, 0) == "semiring_exact"  # int32: exact integer fold

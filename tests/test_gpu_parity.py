@@ -405,6 +405,36 @@ def test_tma_kernels_on_skinny_shapes(mkn, rng):
         assert_bits_equal(got, oracle.product(a32, b32, m, k, n, 0, 2).astype(np.float32))
 
 
+@pytest.mark.parametrize("mkn", [(300, 132, 260), (257, 131, 300)])  # TMA / cp.async kernels
+def test_tropical_accumulate_folds_previous_contents(mkn, rng):
+    """MOA_FLAG_ACCUMULATE on float32 tropical pairs (what the reference-side
+    binding sends, with res prefilled by the identity): the fast folds start
+    from C's contents when the pre-scan of C allows, else the exact loop runs;
+    every case equals the reference's fold into res."""
+    torch = _torch()
+    m, k, n = mkn
+    a = (rng.random(m * k) * 100).astype(np.float32)
+    b = (rng.random(k * n) * 100).astype(np.float32)
+    plan = plan_inner((m, k), (k, n))
+    for comb, red in (("add", "min"), ("add", "max"), ("subtract", "min"), ("subtract", "max")):
+        ops = op_pair(comb, red)
+        c, r = ops.codes()
+        ident = np.float32(ops.reduce_identity)
+        inits = {"identity": np.full(m * n, ident, dtype=np.float32),
+                 "positive": (rng.random(m * n) * 150).astype(np.float32),
+                 "signed": ((rng.random(m * n) - 0.5) * 300).astype(np.float32)}
+        nan = inits["positive"].copy()
+        nan[::97] = np.nan
+        negz = inits["positive"].copy()
+        negz[::89] = -0.0
+        inits.update(nan=nan, negzero=negz)
+        for name, init in inits.items():
+            res = _dev(init.copy())
+            launch(plan, res, _dev(a), _dev(b), ops, accumulate=True)
+            want = oracle.product(a, b, m, k, n, c, r, res=init.astype(np.float64)).astype(np.float32)
+            assert_bits_equal(res.cpu().numpy(), want, f"{ops} init={name}")
+
+
 def test_tropical_tma_strided_rows_odd_k(rng):
     """Round-robin row sets (lda = K*step) keep the TMA-staged tropical kernel
     eligible with an odd K, so its lone-k tail runs; bitwise vs the reference."""

@@ -34,12 +34,12 @@ void trial_tropical(const moa::Problem& p0, float* out, float* ref, unsigned* sp
   p.c = out;
   cudaEvent_t s, e;
   CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
-  CK((moa::tropical_launch<0, 2, 2>(p, special)));
+  CK((moa::tropical_launch<0, 2, 2, false>(p, special)));
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < 2; r++) {
     CK(cudaEventRecord(s));
-    CK((moa::tropical_launch<0, 2, 2>(p, special)));
+    CK((moa::tropical_launch<0, 2, 2, false>(p, special)));
     CK(cudaEventRecord(e)); CK(cudaEventSynchronize(e));
     float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
   }
@@ -62,12 +62,12 @@ void trial_tma(const moa::Problem& p0, float* out, float* ref, unsigned* special
   cudaEvent_t s, e;
   CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
   CK(cudaMemset(out, 0, (size_t)p.M * p.N * 4));
-  CK((moa::tropical_tma_launch<0, 2, 2, MINB, UNR>(p, special)));
+  CK((moa::tropical_tma_launch<0, 2, 2, false, MINB, UNR>(p, special)));
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < 2; r++) {
     CK(cudaEventRecord(s));
-    CK((moa::tropical_tma_launch<0, 2, 2, MINB, UNR>(p, special)));
+    CK((moa::tropical_tma_launch<0, 2, 2, false, MINB, UNR>(p, special)));
     CK(cudaEventRecord(e)); CK(cudaEventSynchronize(e));
     float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
   }
