@@ -70,20 +70,17 @@ template <typename T> __device__ __forceinline__ T safe_div(T x, T y) {
 // rounded quotient: |a - b*q1| < |b| * ulp(q1)/2, q1 not a power of two (whose
 // lower rounding interval is half as wide).  No midpoint can be a quotient of
 // two floating-point numbers, so the test is exact; operands whose exponents
-// could under/overflow any step (|a|, |b| outside [2^-400, 2^400) for double,
-// [2^-40, 2^40) for float), zeros, infinities and NaNs take the IEEE division.
+// could under/overflow any step (|a|, |b| outside [2^-400, 2^400)), zeros,
+// infinities and NaNs take the IEEE division.  (float32 keeps __fdiv_rn: its
+// IEEE division is already cheap.)
 // Either way the result is RN(a/b), bit for bit (tests/test_gpu_parity.py).
 // Kernels prove a whole row of quotients at once and redo the row with the
 // IEEE division when any proof fails, so the common case has no branches.
 __device__ __forceinline__ double rcp_rn(double b) { return __drcp_rn(b); }
-__device__ __forceinline__ float rcp_rn(float b) { return __frcp_rn(b); }
 
 // operand exponent within the reciprocal path's range
 __device__ __forceinline__ bool rcp_range(double x) {
   return ((unsigned)(__double_as_longlong(x) >> 52) & 0x7ffu) - 623u < 800u;  // [2^-400, 2^400)
-}
-__device__ __forceinline__ bool rcp_range(float x) {
-  return ((__float_as_uint(x) >> 23) & 0xffu) - 87u < 80u;  // [2^-40, 2^40)
 }
 // candidate quotient for in-range a, b with y = RN(1/b); ok &= proof that it
 // is RN(a/b).  Out-of-range operands give garbage and must not be used.
@@ -98,42 +95,53 @@ __device__ __forceinline__ double div_candidate(double a, double b, double y, bo
   ok = ok && (uq & 0xfffffffffffffull) != 0 && fabs(r1) < half_ulp_b;
   return q1;
 }
-__device__ __forceinline__ float div_candidate(float a, float b, float y, bool& ok) {
-  const float q0 = __fmul_rn(a, y);
-  const float r0 = __fmaf_rn(-b, q0, a);
-  const float q1 = __fmaf_rn(r0, y, q0);
-  const float r1 = __fmaf_rn(-b, q1, a);
-  const unsigned uq = __float_as_uint(q1);
-  const unsigned eq = (uq >> 23) & 0xffu;  // >= 47 in range
-  const float half_ulp_b = fabsf(b) * __uint_as_float((eq - 24u) << 23);
-  ok = ok && (uq & 0x7fffffu) != 0 && fabsf(r1) < half_ulp_b;
-  return q1;
+
+// int32 division by a reused divisor with a per-divisor multiplier
+// (Granlund & Montgomery 1994, round-up variant, on magnitudes): for d = |y|,
+// l = ceil(log2 d), m = floor(2^32 (2^l - d) / d) + 1, and every 32-bit n,
+// floor(n / d) = (t + ((n - t) >> min(l, 1))) >> max(l - 1, 0) with
+// t = mulhi(m, n).  The sign is applied after (truncating division), |MIN|
+// = 2^31 is a valid n, MIN / -1 wraps to MIN like safe_div, and y = 0 gives 0.
+struct DivMagic32 {
+  uint32_t m;
+  uint32_t sh;  // sh1 | sh2 << 8 | (y == 0) << 16
+};
+__device__ __forceinline__ DivMagic32 div_magic(int32_t y) {
+  const uint32_t d = y < 0 ? 0u - uint32_t(y) : uint32_t(y);
+  if (d == 0) return DivMagic32{0u, 1u << 16};
+  const uint32_t l = d == 1 ? 0u : 32u - __clz(d - 1u);
+  const uint32_t m = uint32_t(((((uint64_t)1 << l) - d) << 32) / d) + 1u;
+  const uint32_t sh1 = l < 1u ? l : 1u, sh2 = l > 0u ? l - 1u : 0u;
+  return DivMagic32{m, sh1 | (sh2 << 8)};
+}
+__device__ __forceinline__ int32_t idiv_magic(int32_t x, uint32_t nx, int32_t y, DivMagic32 g) {
+  const uint32_t t = __umulhi(g.m, nx);
+  const uint32_t q = (t + ((nx - t) >> (g.sh & 0xffu))) >> ((g.sh >> 8) & 0xffu);
+  const uint32_t neg = uint32_t((x ^ y) >> 31);  // all ones when the signs differ
+  const int32_t r = int32_t((q ^ neg) - neg);
+  return (g.sh >> 16) ? 0 : r;
 }
 
-// Integer division by a reused divisor through yr = RN(1/double(y)).
-// q = trunc(x*yr) is exact or, when x/y is an integer, one unit short: for
-// int32 the estimate's error (< |x/y| 2^-51) is below the distance 1/|y| from
-// any non-integer x/y to the next integer.  int64 operands lose bits in the
-// conversion, so the remainder gets one more estimate (|error| < 2^13 after
-// the first).  The last unit is fixed from the exact remainder (truncating
-// division: r = 0 or sign(r) = sign(x) with |r| < |y|), and y = 0, y = -1
-// keep safe_div's results.
-template <typename T>
-__device__ __forceinline__ T idiv_by_rcp(T x, double xd, T y, double yr) {
-  using U = typename IntTraits<T>::U;
-  T q;
-  if constexpr (sizeof(T) == 8) q = T(__double2ll_rz(xd * yr));
-  else q = T(__double2int_rz(xd * yr));
-  T r = wrap_sub(x, wrap_mul(q, y));
-  if constexpr (sizeof(T) == 8) {
-    q = wrap_add(q, T(__double2ll_rz(double(r) * yr)));
-    r = wrap_sub(x, wrap_mul(q, y));
-  }
-  const T s = ((x ^ y) < 0) ? T(-1) : T(1);
-  const U ar = r < 0 ? U(0) - U(r) : U(r), ay = y < 0 ? U(0) - U(y) : U(y);
-  if (r != 0 && ((r < 0) != (x < 0))) q = wrap_sub(q, s);
-  else if (ar >= ay) q = wrap_add(q, s);
-  return y == 0 ? T(0) : (y == T(-1) ? wrap_sub(T(0), x) : q);
+// The same for int64 (64-bit multiplier, 128-bit set-up division per divisor).
+struct DivMagic64 {
+  uint64_t m;
+  uint32_t sh;  // sh1 | sh2 << 8 | (y == 0) << 16
+};
+__device__ __forceinline__ DivMagic64 div_magic(int64_t y) {
+  const uint64_t d = y < 0 ? 0ull - uint64_t(y) : uint64_t(y);
+  if (d == 0) return DivMagic64{0ull, 1u << 16};
+  const uint32_t l = d == 1 ? 0u : 64u - (uint32_t)__clzll((long long)(d - 1ull));
+  const unsigned __int128 num = ((((unsigned __int128)1) << l) - d) << 64;
+  const uint64_t m = uint64_t(num / d) + 1ull;
+  const uint32_t sh1 = l < 1u ? l : 1u, sh2 = l > 0u ? l - 1u : 0u;
+  return DivMagic64{m, sh1 | (sh2 << 8)};
+}
+__device__ __forceinline__ int64_t idiv_magic(int64_t x, uint64_t nx, int64_t y, DivMagic64 g) {
+  const uint64_t t = __umul64hi(g.m, nx);
+  const uint64_t q = (t + ((nx - t) >> (g.sh & 0xffu))) >> ((g.sh >> 8) & 0xffu);
+  const uint64_t neg = uint64_t((x ^ y) >> 63);
+  const int64_t r = int64_t((q ^ neg) - neg);
+  return (g.sh >> 16) ? 0 : r;
 }
 
 template <int C> struct CombineOp;

@@ -91,32 +91,44 @@ __global__ void __launch_bounds__(256) outer_vec_kernel(T* __restrict__ c, const
   const int64_t r0 = blockIdx.y * rows_per_block;
   const int64_t r1 = (r0 + rows_per_block) < M ? (r0 + rows_per_block) : M;
   using A = typename AccType<T, R>::type;
-  if constexpr (C == C_DIV && sizeof(A) == 8) {
+  if constexpr (C == C_DIV && std::is_integral<A>::value) {
+    // the thread's V divisors serve every row of its run: one multiplier each
+    // (div_magic / idiv_magic, moa_common.cuh)
+    using G = decltype(div_magic(A(0)));
+    using U = typename IntTraits<A>::U;
+    G gv[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) gv[q] = div_magic(A(bv[q]));
+#pragma unroll 2
+    for (int64_t i = r0; i < r1; i++) {
+      const A av = A(__ldg(a + i * lda));
+      const U nx = av < 0 ? U(0) - U(av) : U(av);
+      T out[V];
+      if (ACC) ld_32B(cp + i * ldc, out);
+#pragma unroll
+      for (int q = 0; q < V; q++)
+        out[q] = convert<T, A>(ReduceOp<R>::f(A(ACC ? out[q] : ident), idiv_magic(av, nx, A(bv[q]), gv[q])));
+      st_stream_32B(cp + i * ldc, out);
+    }
+  } else if constexpr (C == C_DIV && std::is_same<A, double>::value) {
     // the thread's V divisors are reused by every row of its run: one
-    // reciprocal each (div_candidate / idiv_by_rcp, moa_common.cuh)
+    // reciprocal each (div_candidate, moa_common.cuh)
     double yv[V];
 #pragma unroll
     for (int q = 0; q < V; q++) {
       const double bd = double(A(bv[q]));
-      yv[q] = (std::is_integral<A>::value || rcp_range(bd)) ? rcp_rn(bd)
-                                                            : __longlong_as_double(0x7ff8000000000000ll);
+      yv[q] = rcp_range(bd) ? rcp_rn(bd) : __longlong_as_double(0x7ff8000000000000ll);
     }
 #pragma unroll 2
     for (int64_t i = r0; i < r1; i++) {
       const A av = A(__ldg(a + i * lda));
       A quo[V];
-      if constexpr (std::is_integral<A>::value) {
-        const double xd = double(av);
+      bool ok = rcp_range(av);
 #pragma unroll
-        for (int q = 0; q < V; q++) quo[q] = idiv_by_rcp(av, xd, A(bv[q]), yv[q]);
-      } else {
-        bool ok = rcp_range(av);
+      for (int q = 0; q < V; q++) quo[q] = div_candidate(av, A(bv[q]), yv[q], ok);
+      if (!ok) {
 #pragma unroll
-        for (int q = 0; q < V; q++) quo[q] = div_candidate(av, A(bv[q]), yv[q], ok);
-        if (!ok) {
-#pragma unroll
-          for (int q = 0; q < V; q++) quo[q] = CombineOp<C_DIV>::f(av, A(bv[q]));
-        }
+        for (int q = 0; q < V; q++) quo[q] = CombineOp<C_DIV>::f(av, A(bv[q]));
       }
       T out[V];
       if (ACC) ld_32B(cp + i * ldc, out);

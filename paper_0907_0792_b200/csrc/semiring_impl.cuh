@@ -117,12 +117,12 @@ __global__ void __launch_bounds__(SNT, MINB)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KPair<T>* As = reinterpret_cast<KPair<T>*>(smem_raw);
   KPair<T>* Bs = As + STAGES * Shape::A_STAGE;
-  // division: RN(1/b) (float64) of the current B stage, [BK][BN]; for
-  // float64 NaN where b is outside the reciprocal path's range (so every
-  // proof using it fails), for int64 the reciprocal of double(b).  (int32
-  // keeps the native division: the f64 conversions cost more than they save,
-  // profiles/r01_route_sweep_4096.jsonl.)
-  constexpr bool RCP = C == C_DIV && sizeof(A) == 8;
+  // division: RN(1/b) of the current B stage, [BK][BN], NaN where b is
+  // outside the reciprocal path's range (so every proof using it fails); for
+  // integers the same slots hold each divisor's multiplier and shifts
+  // (div_magic; 8 bytes for int32, 16 for int64).
+  constexpr bool RCP = C == C_DIV && std::is_same<A, double>::value;
+  constexpr bool MAGIC = C == C_DIV && std::is_integral<A>::value;  // staged multipliers
   double* Ys = reinterpret_cast<double*>(Bs + STAGES * Shape::B_STAGE);
 
   // grouped rasterisation: GROUP_M row tiles sweep the column tiles together
@@ -213,9 +213,17 @@ __global__ void __launch_bounds__(SNT, MINB)
       for (int q = 0; q < BK * BN / SNT; q++) {
         const int e = tid + q * SNT, k = e / BN, n = e % BN;
         const double bval = double(reinterpret_cast<const T*>(bs + (k >> 1) * BN + n)[k & 1]);
-        Ys[k * BN + n] = (std::is_integral<A>::value || rcp_range(bval))
-                             ? rcp_rn(bval)
-                             : __longlong_as_double(0x7ff8000000000000ll);
+        Ys[k * BN + n] = rcp_range(bval) ? rcp_rn(bval) : __longlong_as_double(0x7ff8000000000000ll);
+      }
+      __syncthreads();
+    }
+    if constexpr (MAGIC) {
+      using G = decltype(div_magic(A(0)));
+      G* Gs = reinterpret_cast<G*>(Ys);
+#pragma unroll
+      for (int q = 0; q < BK * BN / SNT; q++) {
+        const int e = tid + q * SNT, k = e / BN, n = e % BN;
+        Gs[k * BN + n] = div_magic(A(reinterpret_cast<const T*>(bs + (k >> 1) * BN + n)[k & 1]));
       }
       __syncthreads();
     }
@@ -233,16 +241,19 @@ __global__ void __launch_bounds__(SNT, MINB)
         for (int i = 0; i < TM; i++) av[i] = A(ak[2 * i]);
 #pragma unroll
         for (int j = 0; j < TN; j++) bv[j] = A(bk[2 * 16 * j]);
-        if constexpr (RCP && std::is_integral<A>::value) {
-          double yv[TN];
+        if constexpr (MAGIC) {
+          using G = decltype(div_magic(A(0)));
+          using U = typename IntTraits<A>::U;
+          const G* Gs = reinterpret_cast<const G*>(Ys);
+          G gv[TN];
 #pragma unroll
-          for (int j = 0; j < TN; j++) yv[j] = Ys[kk * BN + 16 * j + tx];
+          for (int j = 0; j < TN; j++) gv[j] = Gs[kk * BN + 16 * j + tx];
 #pragma unroll
           for (int i = 0; i < TM; i++) {
-            const double xd = double(av[i]);
+            const U nx = av[i] < 0 ? U(0) - U(av[i]) : U(av[i]);
 #pragma unroll
             for (int j = 0; j < TN; j++)
-              acc[i][j] = ReduceOp<R>::f(acc[i][j], idiv_by_rcp(av[i], xd, bv[j], yv[j]));
+              acc[i][j] = ReduceOp<R>::f(acc[i][j], idiv_magic(av[i], nx, bv[j], gv[j]));
           }
         } else if constexpr (RCP) {
           // each row's TN quotients from the staged reciprocals, proven
@@ -342,8 +353,12 @@ cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
   using Shape = SemiringShape<T, R, TM, TN, MINB>;
   auto kern = semiring_kernel<T, C, R, ACC, MODEK, TM, TN, MINB>;
   using Acc = typename AccType<T, R>::type;
-  constexpr bool RCP = C == C_DIV && sizeof(Acc) == 8;
-  const size_t smem = Shape::SMEM + (RCP ? (size_t)Shape::BK * Shape::BN * sizeof(double) : 0);
+  // staged reciprocals (float64) or multipliers (integers) for division
+  constexpr size_t stage_elem = C != C_DIV ? 0
+                                : std::is_same<Acc, double>::value ? sizeof(double)
+                                : std::is_same<Acc, int64_t>::value ? sizeof(DivMagic64)
+                                : std::is_same<Acc, int32_t>::value ? sizeof(DivMagic32) : 0;
+  const size_t smem = Shape::SMEM + (size_t)Shape::BK * Shape::BN * stage_elem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + Shape::BM - 1) / Shape::BM;

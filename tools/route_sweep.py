@@ -43,24 +43,35 @@ def main() -> None:
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--out", default="gpurun_out/route_sweep.jsonl")
     ap.add_argument("--only", default=None, help="dtype:combine:reduce, e.g. float64:add:min")
+    ap.add_argument("--outer", action="store_true",
+                    help="outer products (K = 1) of 65536 x 2048 instead (GB/s of result written)")
     args = ap.parse_args()
     n = args.n
     gen = np.random.default_rng(0)
-    plan = plan_inner((n, n), (n, n))
+    if args.outer:
+        from paper_0907_0792_b200.kernel import plan_outer
+        plan = plan_outer((65536,), (2048,))
+    else:
+        plan = plan_inner((n, n), (n, n))
     lines = []
     only = args.only.split(":") if args.only else None
     for dt in (np.float64, np.float32, np.int32, np.int64):
         if only and np.dtype(dt).name != only[0]:
             continue
-        a, b = operands(dt, n, gen)
-        res = torch.empty(n * n, dtype=a.dtype, device="cuda")
+        if args.outer:
+            a, b = operands(dt, 256, gen)
+            a, b = a[:plan.noproc], b[:plan.elsinop]
+        else:
+            a, b = operands(dt, n, gen)
+        res = torch.empty(plan.noproc * plan.elsinop, dtype=a.dtype, device="cuda")
         for comb in moa.COMBINE_OPS:
             for red in moa.REDUCE_OPS:
                 if only and (comb, red) != (only[1], only[2]):
                     continue
                 ops = moa.op_pair(comb, red)
                 c, r = ops.codes()
-                kern = _native.plan_kernel(native_dtype(np.dtype(dt)), n, n, n, c, r, 0)
+                kern = _native.plan_kernel(native_dtype(np.dtype(dt)), plan.noproc, plan.rowsinred,
+                                           plan.elsinop, c, r, 0)
                 launch(plan, res, a, b, ops)
                 torch.cuda.synchronize()
                 best = float("inf")
@@ -74,6 +85,11 @@ def main() -> None:
                 rec = {"dtype": np.dtype(dt).name, "combine": comb, "reduce": red, "kernel": kern,
                        "n": n, "ms": round(best, 4),
                        "Gpairs_s": round(n ** 3 / (best * 1e-3) / 1e9, 1)}
+                if args.outer:
+                    nbytes = plan.noproc * plan.elsinop * np.dtype(dt).itemsize
+                    rec = {"dtype": np.dtype(dt).name, "combine": comb, "reduce": red,
+                           "kernel": "outer", "M": plan.noproc, "N": plan.elsinop,
+                           "ms": round(best, 4), "GB_s": round(nbytes / (best * 1e-3) / 1e9, 1)}
                 lines.append(rec)
                 print(json.dumps(rec), flush=True)
         del a, b, res
