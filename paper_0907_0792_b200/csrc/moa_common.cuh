@@ -260,9 +260,19 @@ __host__ __device__ inline bool fast_fold_is_exact(int combine, unsigned fa, uns
 // 1 = FMNMX3 on floats, 2 = VIMNMX3 on the bit patterns.  Mode 2 needs every
 // combine result to be a non-negative, non-NaN float, for which unsigned
 // integer order equals float order (and +-0 ties cannot occur): true for
-// add of two sign-clear, NaN-free operands.  VIMNMX3 issues faster beside
-// FADD2 than FMNMX3 does (profiles/r01_minplus_mix2.json).
+// add of two sign-clear, NaN-free operands (and for multiply, below).
+// VIMNMX3 issues faster beside FADD2 than FMNMX3 does
+// (profiles/r01_minplus_mix2.json).
 __host__ __device__ inline int tropical_fold_mode(int combine, unsigned fa, unsigned fb) {
+  if (combine == C_MUL) {
+    // max-times / min-times: only the unsigned-order fold, for sign-clear,
+    // NaN-free operands without a 0 x inf pair (every product is then a
+    // non-negative non-NaN float; underflow gives +0)
+    constexpr unsigned Z = S_PZERO | S_NZERO, I = S_PINF | S_NINF;
+    if ((fa | fb) & (S_NAN | S_NEG)) return 0;
+    if (((fa & Z) && (fb & I)) || ((fa & I) && (fb & Z))) return 0;
+    return 2;
+  }
   if (!fast_fold_is_exact(combine, fa, fb)) return 0;
   if (combine == C_ADD && !((fa | fb) & (S_NAN | S_NEG))) return 2;
   return 1;

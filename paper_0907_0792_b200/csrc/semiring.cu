@@ -13,7 +13,7 @@ cudaError_t launch_semiring_i64(const Problem& p);
 
 bool semiring_fast_candidate(int dtype, int combine, int reduce, bool accumulate) {
   (void)accumulate;  // accumulate folds C's contents too; the pre-scan covers them
-  return dtype == MOA_DTYPE_F32 && (combine == C_ADD || combine == C_SUB) &&
+  return dtype == MOA_DTYPE_F32 && (combine == C_ADD || combine == C_SUB || combine == C_MUL) &&
          (reduce == R_MIN || reduce == R_MAX);
 }
 

@@ -380,7 +380,8 @@ cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
 namespace moa {
 namespace {
 
-// float32 tropical pair: pre-scan A (M x K, lda), B (K x N, ldb) and, when
+// float32 tropical pair ((add|sub|mul) x (min|max); multiply only with the
+// unsigned-order fold): pre-scan A (M x K, lda), B (K x N, ldb) and, when
 // accumulating, C (M x N, ldc) for NaN / +-inf / +-0 / sign, then launch one
 // specialisation per fold mode; all but the one the flags select exit at once.
 template <int C, int R, bool ACC>
@@ -393,8 +394,10 @@ cudaError_t tropical_candidate(const Problem& p) {
     launch_scan<float>(static_cast<const float*>(p.a), p.M, p.K, p.lda, special, p.stream);
     launch_scan<float>(static_cast<const float*>(p.b), p.K, p.N, p.ldb, special + 1, p.stream);
     if (ACC) launch_scan<float>(static_cast<const float*>(p.c), p.M, p.N, p.ldc, special + 2, p.stream);
-    if constexpr (C == C_ADD) e = tropical_launch<C, R, 2, ACC>(p, special);
-    if (e == cudaSuccess) e = tropical_launch<C, R, 1, ACC>(p, special);
+    if constexpr (C == C_ADD || C == C_MUL) e = tropical_launch<C, R, 2, ACC>(p, special);
+    if constexpr (C != C_MUL) {
+      if (e == cudaSuccess) e = tropical_launch<C, R, 1, ACC>(p, special);
+    }
     if (e == cudaSuccess) e = semiring_launch<float, C, R, ACC, 0>(p, special);
   }
   cudaError_t e2 = cudaFreeAsync(special, p.stream);
@@ -403,7 +406,7 @@ cudaError_t tropical_candidate(const Problem& p) {
 
 template <typename T, int C, int R>
 cudaError_t semiring_acc(const Problem& p) {
-  constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB) &&
+  constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB || C == C_MUL) &&
                         (R == R_MIN || R == R_MAX);
   if constexpr (cand) {
     return p.accumulate ? tropical_candidate<C, R, true>(p) : tropical_candidate<C, R, false>(p);

@@ -1,5 +1,6 @@
-// K2 fast loops for the float32 tropical semirings — combine in {add, subtract},
-// reduce in {min, max} (BASELINE config 5) — in their own kernel.
+// K2 fast loops for the float32 tropical semirings — combine in {add, subtract}
+// (BASELINE config 5) or multiply (max-times / min-times, non-negative data
+// only), reduce in {min, max} — in their own kernels.
 //
 // Two kernels share the loop: tropical_tma_kernel (16-byte aligned rows:
 // TMA-staged tiles, mbarrier pipeline, no block barrier in the main loop) and
@@ -45,6 +46,10 @@ __device__ __forceinline__ unsigned long long pair_op_bcast(float x0, float x1, 
   if (C == C_SUB)  // combine(a, b) = a - b, A element first (_ckernel.pyx:71)
     asm("{\n\t.reg .b64 ta, tb;\n\tmov.b64 ta, {%1, %1};\n\tmov.b64 tb, {%2, %3};\n\t"
         "sub.rn.f32x2 %0, ta, tb;\n\t}"
+        : "=l"(r) : "f"(a), "f"(x0), "f"(x1));
+  else if (C == C_MUL)
+    asm("{\n\t.reg .b64 ta, tb;\n\tmov.b64 ta, {%1, %1};\n\tmov.b64 tb, {%2, %3};\n\t"
+        "mul.rn.f32x2 %0, tb, ta;\n\t}"
         : "=l"(r) : "f"(a), "f"(x0), "f"(x1));
   else
     asm("{\n\t.reg .b64 ta, tb;\n\tmov.b64 ta, {%1, %1};\n\tmov.b64 tb, {%2, %3};\n\t"

@@ -378,6 +378,38 @@ def test_tropical_fast_and_exact_loops_agree(dt, mkn, rng):
                 assert_bits_equal(got, want, f"{ops} poison={poison}")
 
 
+@pytest.mark.parametrize("mkn", [(300, 132, 260), (257, 131, 300)])  # TMA / cp.async kernels
+def test_max_times_fast_fold(mkn, rng):
+    """float32 (multiply, min|max): non-negative data runs the FMUL2 +
+    unsigned-order fold; zeros with infinities (0 x inf = NaN), negative
+    values, -0 and NaN fall back to the exact loop.  Bitwise vs the reference."""
+    m, k, n = mkn
+    base_a = rng.random(m * k).astype(np.float32) * np.float32(3)
+    base_b = rng.random(k * n).astype(np.float32) * np.float32(3)
+    base_a[rng.random(m * k) < 0.03] = 0.0
+    base_b[rng.random(k * n) < 0.03] = 1e-30  # products that underflow to +0
+    for red in ("max", "min"):
+        ops = op_pair("multiply", red)
+        c, r = ops.codes()
+        for poison in (None, "inf_and_zero", "negative", "negzero", "nan", "inf_only"):
+            a, b = base_a.copy(), base_b.copy()
+            if poison == "inf_and_zero":
+                b[::53] = np.inf
+            elif poison == "negative":
+                a[::7] *= -1
+            elif poison == "negzero":
+                a[::41] = -0.0
+            elif poison == "nan":
+                b[::61] = np.nan
+            elif poison == "inf_only":
+                a[a == 0] = 0.5
+                b[::53] = np.inf
+            want = oracle.product(a, b, m, k, n, c, r).astype(np.float32)
+            got = moa.inner(MoaArray((m, k), a, dtype=np.float32), MoaArray((k, n), b, dtype=np.float32),
+                            ops).data
+            assert_bits_equal(got, want, f"{ops} poison={poison}")
+
+
 @pytest.mark.parametrize("mkn", [(20000, 48, 8), (12000, 4, 4), (9600, 132, 16), (12000, 2, 2)])
 def test_tma_kernels_on_skinny_shapes(mkn, rng):
     """Boxes wider than the matrix (N below the 16/128-column TMA box, K below
