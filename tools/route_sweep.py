@@ -17,6 +17,7 @@ from __future__ import annotations
 import argparse
 import json
 import sys
+import time
 from pathlib import Path
 
 import numpy as np
@@ -94,6 +95,7 @@ def main() -> None:
                 print(json.dumps(rec), flush=True)
         del a, b, res
         torch.cuda.empty_cache()
+        time.sleep(3)  # let clocks/power settle between dtype groups
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text("".join(json.dumps(x) + "\n" for x in lines))
 
