@@ -218,9 +218,19 @@ template <> struct ReduceOp<R_MAX> {
 // it stays in float32.  Sums and products of many terms do not commute with
 // rounding, so add/multiply reduces on float32 storage run in float64.
 // ---------------------------------------------------------------------------
-template <typename T, int R> struct AccType { using type = T; };
-template <> struct AccType<float, R_ADD> { using type = double; };
-template <> struct AccType<float, R_MUL> { using type = double; };
+// Accumulation/computation type.  float32 data reproduces the reference's
+// float64 arithmetic rounded once: sums and products of the fold need float64;
+// a min/max fold can stay in float32 (rounding is monotone) only when no
+// combine result that is nonzero in float64 can round to a signed zero in
+// float32 — true for add/subtract/min/max, not for multiply/divide, whose
+// underflow would turn max(-tiny, +0) = +0 into a -0/+0 tie.
+template <typename T, int C, int R> struct AccType { using type = T; };
+template <int C> struct AccType<float, C, R_ADD> { using type = double; };
+template <int C> struct AccType<float, C, R_MUL> { using type = double; };
+template <> struct AccType<float, C_MUL, R_MIN> { using type = double; };
+template <> struct AccType<float, C_MUL, R_MAX> { using type = double; };
+template <> struct AccType<float, C_DIV, R_MIN> { using type = double; };
+template <> struct AccType<float, C_DIV, R_MAX> { using type = double; };
 
 template <typename To, typename From> __device__ __forceinline__ To convert(From x) { return To(x); }
 template <> __device__ __forceinline__ float convert<float, double>(double x) { return __double2float_rn(x); }

@@ -70,7 +70,7 @@ __device__ __forceinline__ void ld_32B(const float* p, float (&v)[8]) {
 // one result element: reduce(init, combine(a, b)) in the accumulation type
 template <typename T, int C, int R>
 __device__ __forceinline__ T outer_elem(T av, T bv, T init) {
-  using A = typename AccType<T, R>::type;
+  using A = typename AccType<T, C, R>::type;
   A v = CombineOp<C>::f(A(av), A(bv));
   return convert<T, A>(ReduceOp<R>::f(A(init), v));
 }
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) outer_vec_kernel(T* __restrict__ c, const
   T* cp = c + jv * V;
   const int64_t r0 = blockIdx.y * rows_per_block;
   const int64_t r1 = (r0 + rows_per_block) < M ? (r0 + rows_per_block) : M;
-  using A = typename AccType<T, R>::type;
+  using A = typename AccType<T, C, R>::type;
   if constexpr (C == C_DIV && std::is_integral<A>::value) {
     // the thread's V divisors serve every row of its run: one multiplier each
     // (div_magic / idiv_magic, moa_common.cuh)

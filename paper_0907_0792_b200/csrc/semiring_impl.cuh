@@ -44,9 +44,9 @@ constexpr int SNT = 256, GROUP_M = 8;  // 16 x 16 threads per CTA
 
 template <typename T> struct alignas(2 * sizeof(T)) KPair { T x, y; };
 
-template <typename T, int R, int TM_, int TN_, int MINB_>
+template <typename T, int C, int R, int TM_, int TN_, int MINB_>
 struct SemiringShape {
-  static constexpr bool F4 = sizeof(typename AccType<T, R>::type) == 4;
+  static constexpr bool F4 = sizeof(typename AccType<T, C, R>::type) == 4;
   static constexpr int TM = TM_, TN = TN_;
   static constexpr int BM = 16 * TM, BN = 16 * TN;
   static constexpr int BK = F4 ? 32 : 16;       // k per stage (one barrier per BK)
@@ -64,8 +64,8 @@ struct SemiringShape {
 
 // Default tiles: float32 min/max (c5): 8x8 per thread, two CTAs per SM
 // (tools/tune_semiring.cu); float64 or float64-accumulated: 8x8, one CTA.
-template <typename T, int R> struct DefaultTile {
-  static constexpr bool F4 = sizeof(typename AccType<T, R>::type) == 4;
+template <typename T, int C, int R> struct DefaultTile {
+  static constexpr bool F4 = sizeof(typename AccType<T, C, R>::type) == 4;
   static constexpr int TM = 8, TN = 8, MINB = F4 ? 2 : 1;
 };
 
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(SNT, MINB)
     semiring_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ b,
                     int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                     const unsigned* special, int64_t tiles_m, int64_t tiles_n) {
-  using A = typename AccType<T, R>::type;
-  using Shape = SemiringShape<T, R, TM, TN, MINB>;
+  using A = typename AccType<T, C, R>::type;
+  using Shape = SemiringShape<T, C, R, TM, TN, MINB>;
   constexpr int STAGES = Shape::STAGES, BM = Shape::BM, BN = Shape::BN;
   constexpr int BK = Shape::BK, KP = Shape::KP;
   if constexpr (MODEK >= 0) {
@@ -274,6 +274,14 @@ __global__ void __launch_bounds__(SNT, MINB)
 #pragma unroll
             for (int j = 0; j < TN; j++) acc[i][j] = ReduceOp<R>::f(acc[i][j], q[j]);
           }
+        } else if constexpr (std::is_same<T, float>::value && C == C_MUL && R == R_ADD) {
+          // float32 data accumulated in float64: the product of two floats is
+          // exact in float64, so RN(acc + RN(a*b)) = RN(acc + a*b) = DFMA
+          // (one FP64 instruction per pair instead of two, same bits)
+#pragma unroll
+          for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < TN; j++) acc[i][j] = __fma_rn(av[i], bv[j], acc[i][j]);
         } else if constexpr (std::is_same<A, int32_t>::value && (C == C_ADD || C == C_SUB) &&
                              (R == R_MIN || R == R_MAX)) {
           // int32 tropical: one DPX add-then-min/max (VIADDMNMX) per pair;
@@ -347,12 +355,12 @@ void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* o
   count_launch();
 }
 
-template <typename T, int C, int R, bool ACC, int MODEK, int TM = DefaultTile<T, R>::TM,
-          int TN = DefaultTile<T, R>::TN, int MINB = DefaultTile<T, R>::MINB>
+template <typename T, int C, int R, bool ACC, int MODEK, int TM = DefaultTile<T, C, R>::TM,
+          int TN = DefaultTile<T, C, R>::TN, int MINB = DefaultTile<T, C, R>::MINB>
 cudaError_t semiring_launch(const Problem& p, const unsigned* special) {
-  using Shape = SemiringShape<T, R, TM, TN, MINB>;
+  using Shape = SemiringShape<T, C, R, TM, TN, MINB>;
   auto kern = semiring_kernel<T, C, R, ACC, MODEK, TM, TN, MINB>;
-  using Acc = typename AccType<T, R>::type;
+  using Acc = typename AccType<T, C, R>::type;
   // staged reciprocals (float64) or multipliers (integers) for division
   constexpr size_t stage_elem = C != C_DIV ? 0
                                 : std::is_same<Acc, double>::value ? sizeof(double)

@@ -190,6 +190,26 @@ def test_ragged_shapes_all_pairs_vs_port(mkn, rng):
             assert_bits_equal(got, want, f"{mkn} {ops}")
 
 
+@pytest.mark.parametrize("mkn", [(129, 33, 130), (300, 41, 257)])
+def test_float32_all_pairs_with_specials_vs_port(mkn, rng):
+    """float32 storage, every pair, data with zeros, infinities, NaN and
+    subnormals: the reference's float64 result rounded once, bit for bit
+    (including (multiply, add), which runs as DFMA on exact float products)."""
+    m, k, n = mkn
+    a = ((rng.random(m * k) * 3 - 1) * 10.0 ** rng.integers(-3, 4, m * k)).astype(np.float32)
+    b = ((rng.random(k * n) * 3 - 1) * 10.0 ** rng.integers(-3, 4, k * n)).astype(np.float32)
+    for x in (a, b):
+        idx = rng.choice(x.size, size=x.size // 20, replace=False)
+        x[idx] = rng.choice(np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -3e-39],
+                                     dtype=np.float32), size=idx.size)
+    for ops in _pairs_sample():
+        c, r = ops.codes()
+        want = oracle.product(a, b, m, k, n, c, r).astype(np.float32)
+        got = moa.inner(MoaArray((m, k), a, dtype=np.float32), MoaArray((k, n), b, dtype=np.float32),
+                        ops).data
+        assert_bits_equal(got, want, f"{mkn} {ops}")
+
+
 def test_round_robin_row_sets_fill_the_same_result(rng):
     """Worker k of W launching rows k::W into one buffer == one full launch
     (parallel.py:38-42 on the device), for every kernel route."""
