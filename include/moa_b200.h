@@ -112,9 +112,11 @@ uint64_t moa_launch_count(void);
 /*
  * Which kernel moa_product_rows would run for these arguments, as a static
  * string ("outer", "fill", "dmma", "semiring_exact", "semiring_fast", "none").
- * Host-only; launches nothing.  "semiring_fast" means the kernel that decides
- * on the device, after a NaN/-0/inf pre-scan of the operands, whether the
- * 3-input min/max fast loop is bit-exact for this data.
+ * Host-only; launches nothing.  "semiring_fast" (float32 (add|subtract|
+ * multiply) x (min|max), with or without MOA_FLAG_ACCUMULATE) means the
+ * kernels that decide on the device, after a NaN/+-0/inf/sign pre-scan of the
+ * operands (and of res when accumulating), whether a packed fast fold is
+ * bit-exact for this data; otherwise the exact fold runs.
  */
 const char* moa_plan_kernel(int dtype, int64_t noproc, int64_t rowsinred,
                             int64_t elsinop, int combine_code, int reduce_code,
