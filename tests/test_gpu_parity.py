@@ -245,6 +245,41 @@ def test_outer_row_sets(rng):
     assert_bits_equal(full.cpu().numpy(), (np.multiply.outer(a, b) + 0.0).ravel())
 
 
+@pytest.mark.parametrize("dt", [np.float64, np.float32, np.int32, np.int64])
+@pytest.mark.parametrize("mn", [(300, 512), (301, 70), (64, 9)])  # vec / scalar / flat kernels
+def test_outer_kernels_every_dtype_and_accumulate(dt, mn, rng):
+    """The three outer-product kernels for every element type, write-only and
+    accumulating, all 24 pairs: the reference's fold of one term into res."""
+    torch = _torch()
+    m, n = mn
+    if np.dtype(dt).kind == "i":
+        a = rng.integers(-50, 50, m).astype(dt)
+        b = rng.integers(-50, 50, n).astype(dt)
+        init = rng.integers(-50, 50, m * n).astype(dt)
+    else:
+        a = ((rng.random(m) * 3 - 1) * 10.0 ** rng.integers(-2, 3, m)).astype(dt)
+        b = ((rng.random(n) * 3 - 1) * 10.0 ** rng.integers(-2, 3, n)).astype(dt)
+        b[::17] = 0.0
+        init = (rng.random(m * n) * 3 - 1).astype(dt)
+    plan = plan_outer((m,), (n,))
+    for ops in _pairs_sample():
+        c, r = ops.codes()
+        for acc in (False, True):
+            res = _dev(init.copy()) if acc else torch.empty(m * n, dtype=_dev(a).dtype, device="cuda")
+            launch(plan, res, _dev(a), _dev(b), ops, accumulate=acc)
+            got = res.cpu().numpy()
+            if np.dtype(dt).kind == "i":
+                wi = oracle.product(a.astype(np.float64), b.astype(np.float64), m, 1, n, c, r,
+                                    res=init.astype(np.float64) if acc else None)
+                if c == 3:  # integer division truncates (x/0 = 0); compare on the exact cases
+                    continue
+                np.testing.assert_array_equal(got, wi.astype(dt), err_msg=f"{ops} acc={acc}")
+            else:
+                want = oracle.product(a, b, m, 1, n, c, r,
+                                      res=init.astype(np.float64) if acc else None)
+                assert_bits_equal(got, want.astype(dt), f"{np.dtype(dt).name} {ops} acc={acc}")
+
+
 def test_accumulate_mode_matches_reference_semantics(rng):
     """MOA_FLAG_ACCUMULATE folds into res's contents, like _ckernel.product_rows."""
     torch = _torch()
