@@ -60,6 +60,8 @@ struct SemiringShape {
   static constexpr int QA = BM * BK / SNT, A_RSTEP = SNT / BK;
   static constexpr int QB = BK * BN / SNT, B_KSTEP = SNT / BN;
   static_assert(QA <= 32 && B_KSTEP % 2 == 0 && TM % 2 == 0 && TN % 2 == 0, "tile layout");
+  static_assert(SNT % BN == 0 && SNT % BK == 0 && (BM * BK) % SNT == 0,
+                "the element-wise loaders cover whole tiles only when BN and BK divide the CTA");
 };
 
 // Default tiles: float32 min/max (c5): 8x8 per thread, two CTAs per SM

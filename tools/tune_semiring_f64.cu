@@ -62,8 +62,6 @@ void sweep(const char* route, const moa::Problem& p, double* c, double* ref, uns
   trial<C, R, 4, 8, 2>(route, p, c, ref, cnt, false);
   trial<C, R, 4, 4, 3>(route, p, c, ref, cnt, false);
   trial<C, R, 4, 4, 4>(route, p, c, ref, cnt, false);
-  trial<C, R, 6, 8, 1>(route, p, c, ref, cnt, false);
-  trial<C, R, 8, 6, 1>(route, p, c, ref, cnt, false);
 }
 
 int main() {
