@@ -168,6 +168,28 @@ def main() -> None:
             b = rng.integers(-1000, 1001, size=k * n).astype(dt)
             add("inner", ops, (m, k), a, (k, n), b, "int_medium", dtype=dt)
 
+    # float32 inputs whose products/quotients under- or overflow float32 (but
+    # not float64), with both signs, zeros and subnormals: the float32 result
+    # must still be the reference's float64 fold rounded once (signed-zero ties
+    # from float32 underflow must not leak in).  Appended last so the earlier
+    # cases keep their indices.
+    for ops in pairs:
+        m, k, n = 17, 29, 19
+        a = ((rng.random(m * k) * 2 - 1) * 10.0 ** rng.integers(-30, 31, m * k)).astype(np.float32)
+        b = ((rng.random(k * n) * 2 - 1) * 10.0 ** rng.integers(-30, 31, k * n)).astype(np.float32)
+        a[rng.random(m * k) < 0.05] = 0.0
+        b[rng.random(k * n) < 0.05] = -0.0
+        a[rng.random(m * k) < 0.03] = 1e-45
+        b[rng.random(k * n) < 0.03] = -3e-39
+        add("inner", ops, (m, k), a, (k, n), b, "f32_underflow", dtype=np.float32)
+    for red in ("max", "min"):  # max-times on non-negative data with tiny values
+        ops = mp.op_pair("multiply", red)
+        m, k, n = 40, 33, 36
+        a = (rng.random(m * k) * 10.0 ** rng.integers(-25, 5, m * k)).astype(np.float32)
+        b = (rng.random(k * n) * 10.0 ** rng.integers(-25, 5, k * n)).astype(np.float32)
+        a[rng.random(m * k) < 0.05] = 0.0
+        add("inner", ops, (m, k), a, (k, n), b, "f32_maxtimes", dtype=np.float32)
+
     arrays = {}
     for i, (mode, c, r, sa, a, sb, b, out, oshape, tag) in enumerate(cases):
         meta = [0 if mode == "inner" else 1, c, r, len(sa), *sa, len(sb), *sb]
