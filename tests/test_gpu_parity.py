@@ -748,12 +748,14 @@ def test_integer_tropical_wraps(rng):
             np.testing.assert_array_equal(got, want, err_msg=f"{np.dtype(dt).name} {comb}/{red}")
 
 
-def test_k_chunked_accumulation_replays_one_pass(rng):
+@pytest.mark.parametrize("mkn", [(700, 1000, 520),    # cp.async kernels
+                                 (2000, 1000, 520)])  # TMA kernel (>= 148 64x64 tiles)
+def test_k_chunked_accumulation_replays_one_pass(mkn, rng):
     """Accumulating k-chunks (slab-aligned) with MOA_FLAG_ACCUMULATE gives the
     bits of one DMMA pass — what the pipelined broadcast of B relies on."""
     torch = _torch()
     from paper_0907_0792_b200.distributed import k_chunks
-    m, k, n = 700, 1000, 520
+    m, k, n = mkn
     a, b = _dev(rng.random(m * k) * 2 - 1), _dev(rng.random(k * n) * 2 - 1)
     one = torch.empty(m * n, dtype=torch.float64, device="cuda")
     launch(plan_inner((m, k), (k, n)), one, a, b, moa.MUL_ADD)
