@@ -324,10 +324,16 @@ def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, c
                       *, exact: bool = False, device=None) -> MoaArray:
     """Host operands -> host result with copies overlapped with compute.
 
-    B goes to the device first (every row needs it); then for each row block:
-    H2D of its A rows on a copy stream, the kernel on the compute stream, D2H
-    of its C rows on a second copy stream, with two-deep device buffers.
+    For each row block: H2D of its A rows on a copy stream, the kernel on the
+    compute stream, D2H of its C rows on a second copy stream, with two-deep
+    device buffers.  Every row needs all of B, so a host B is copied in
+    slab-aligned k-chunks behind the first block's A rows, and the first
+    block is computed chunk by chunk as they land (later chunks accumulate,
+    MOA_FLAG_ACCUMULATE; the same k order, so the same bits, whenever the fold
+    is stored in its own type) — B's transfer then hides behind compute
+    instead of preceding it.
     """
+    from .distributed import k_chunks  # local: distributed imports this module
     from .parallel import row_blocks  # local: parallel imports this module
     torch = _torch()
     _native.load()
@@ -338,9 +344,26 @@ def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, c
     m, n, lda = plan.noproc, plan.elsinop, plan.lstride
     comp = torch.cuda.current_stream(dev)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    b_dev = stage(b, dev, dtype)
     out = torch.empty(m * n, dtype=tdt, pin_memory=True)
     blocks = [r for r in row_blocks(m, chunks) if len(r)]
+    k = plan.rowsinred
+    # k-chunks accumulate through the result buffer, so the fold must not be
+    # carried in a wider type than it is stored in (float32 data folded in
+    # float64: sums, products, and multiply/divide with min/max)
+    wide = np.dtype(dtype) == np.float32 and (ops.reduce_name in ("add", "multiply") or
+                                              ops.combine_name in ("multiply", "divide"))
+    chunked = not b.is_device and not wide
+    b_chunks = k_chunks(k, len(blocks)) if chunked else [(0, k)]
+    if not chunked:
+        b_dev = stage(b, dev, dtype)
+        b_ready = [None]
+    else:
+        b_dev = torch.empty(k * n, dtype=tdt, device=dev)
+        host_b = b.data if b.data.dtype == dtype else b.data.astype(dtype)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            host_b_t = torch.from_numpy(host_b)
+        b_ready = []
     rows_max = max(len(r) for r in blocks)
     a_buf = [torch.empty(rows_max * lda, dtype=tdt, device=dev) for _ in range(2)]
     c_buf = [torch.empty(rows_max * n, dtype=tdt, device=dev) for _ in range(2)]
@@ -359,12 +382,27 @@ def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, c
             a_buf[slot][:na].copy_(host_a_t[r0 * lda:r1 * lda], non_blocking=True)
             a_ready = torch.cuda.Event()
             a_ready.record(s_in)
+            if idx == 0 and chunked:  # B's k-chunks queue behind block 0's rows
+                for k0, k1 in b_chunks:
+                    b_dev[k0 * n:k1 * n].copy_(host_b_t[k0 * n:k1 * n], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(s_in)
+                    b_ready.append(ev)
         comp.wait_event(a_ready)
         if c_free[slot] is not None:
             comp.wait_event(c_free[slot])
-        sub = KernelPlan(plan.mode, r1 - r0, plan.rowsinred, n, lda, plan.rstride, plan.restride,
-                         plan.result_shape)
-        launch(sub, c_buf[slot][:nc], a_buf[slot][:na], b_dev, ops, exact=exact, stream=comp)
+        if idx == 0:
+            for j, (k0, k1) in enumerate(b_chunks):
+                if b_ready[j] is not None:
+                    comp.wait_event(b_ready[j])
+                part = KernelPlan(plan.mode, r1 - r0, k1 - k0, n, lda, plan.rstride, plan.restride,
+                                  plan.result_shape)
+                launch(part, c_buf[slot][:nc], a_buf[slot][k0:na], b_dev[k0 * n:], ops,
+                       exact=exact, accumulate=j > 0, stream=comp)
+        else:
+            sub = KernelPlan(plan.mode, r1 - r0, k, n, lda, plan.rstride, plan.restride,
+                             plan.result_shape)
+            launch(sub, c_buf[slot][:nc], a_buf[slot][:na], b_dev, ops, exact=exact, stream=comp)
         done = torch.cuda.Event()
         done.record(comp)
         a_free[slot] = done

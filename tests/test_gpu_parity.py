@@ -653,8 +653,11 @@ def test_streamed_host_path_bitwise_equals_one_launch(rng):
     m, k, n = 1000, 300, 777
     a = rng.random(m * k) * 2 - 1
     b = rng.random(k * n) * 2 - 1
+    # float64 / fast-fold float32 pairs stream B in k-chunks (accumulating);
+    # float32 pairs folded in float64 take B in one piece
     for ops, dt in ((op_pair("multiply", "add"), np.float64), (op_pair("add", "min"), np.float32),
-                    (op_pair("max", "multiply"), np.float64)):
+                    (op_pair("max", "multiply"), np.float64), (op_pair("divide", "max"), np.float64),
+                    (op_pair("multiply", "add"), np.float32), (op_pair("subtract", "max"), np.float32)):
         A, B = MoaArray((m, k), a, dtype=dt), MoaArray((k, n), b, dtype=dt)
         want = moa.inner(A.to_device(), B.to_device(), ops).host_data()
         for chunks in (2, 3, 7):
