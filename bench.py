@@ -396,7 +396,8 @@ def measure_e2e(w, rows_range, a_pin, b_pin, steps, warmup, device, world, rank,
 
 
 # ---------------------------------------------------------------------------- CPU legs
-def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 500, rows: int | None = None):
+def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 500, rows: int | None = None,
+                       min_reps: int = 3):
     """Reference hot loop (oracle/_ref, else the C port) on all host cores.
 
     Returns (seconds per unit of ``rows`` rows, kind, cores, sample description)."""
@@ -412,7 +413,7 @@ def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 500, row
         (lambda: oracle.product(a_s, b, rows, k, n, comb, red, workers=cores))
     times = []
     t_end = time.perf_counter() + budget_s
-    while len(times) < max_reps and (len(times) < 3 or time.perf_counter() < t_end):
+    while len(times) < max_reps and (len(times) < min_reps or time.perf_counter() < t_end):
         t0 = time.perf_counter()
         run()
         times.append(time.perf_counter() - t0)
@@ -580,6 +581,14 @@ def main() -> None:
                           "kernel_ms": round(d["kernel_ms_mean"], 4),
                           "roofline": roofline(wi, mi, d["kernel_ms_mean"]),
                           "clocks": d["clocks"]}
+            if rank == 0 and not args.no_cpu:
+                # the reference's own loop on a small row sample (~1-3 s of CPU)
+                rows_i = {"c1": mi, "c3": 1024, "c4": 32, "c5": 32}[key]
+                t_i, kind_i, cores_i, sample_i, rows_i = cpu_reference_time(
+                    wi, ai, bi, budget_s=1.5, rows=rows_i, min_reps=1)
+                inner[key]["cpu_baseline"] = {
+                    "value": round(to_unit(wi, unit_amount(wi, rows_i), t_i), 4),
+                    "unit": METRIC[key][1], "cores": cores_i, "kind": kind_i, "sample": sample_i}
             del ai, bi
         line["inner"] = inner
 
