@@ -94,7 +94,8 @@ void trial(const char* cname, const Shape& sh, double* A, double* B, double* C, 
 }
 
 int main() {
-  std::vector<Shape> shapes = {{"c1", 256, 256, 256}, {"c1b", 256, 256, 256}};
+  std::vector<Shape> shapes = {{"c1", 256, 256, 256}, {"m1k", 1024, 1024, 1024},
+                               {"c3", 32768, 256, 4096}, {"c4", 16384, 16384, 16384}};
   for (const Shape& sh : shapes) {
     double *A, *B, *C, *Cref;
     unsigned long long* d_cnt;
@@ -103,14 +104,13 @@ int main() {
     CK(cudaMalloc(&d_cnt, 8));
     fill_uniform<<<1184, 256>>>(A, sh.M * sh.K, 1); fill_uniform<<<1184, 256>>>(B, sh.K * sh.N, 2);
     using namespace moa;
-    trial<DmmaCfg<32, 32, 16, 16, 3, 32, 1>>("32x32_small", sh, A, B, C, Cref, d_cnt, true);
-    trial<DmmaCfg<16, 32, 16, 8, 3, 32, 1>>("16x32_w16x8", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<16, 32, 16, 8, 4, 32, 1>>("16x32_w16x8_s4", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<16, 32, 16, 8, 2, 32, 1>>("16x32_w16x8_s2", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<16, 32, 16, 8, 3, 64, 1>>("16x32_w16x8_bk64", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<16, 32, 16, 8, 5, 16, 1>>("16x32_w16x8_bk16_s5", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<16, 32, 16, 8, 3, 32, 1, true>>("16x32_w16x8_pf", sh, A, B, C, Cref, d_cnt, false);
-    trial<DmmaCfg<16, 64, 16, 8, 3, 32, 1>>("16x64_w16x8", sh, A, B, C, Cref, d_cnt, false);
+    // reference bits: the cp.async large tile; every other config must match them
+    trial<DmmaCfg<64, 128, 32, 32, 4, 16, 2, false, 16>>("cp_64x128_s4_2cta_g16", sh, A, B, C, Cref, d_cnt, true);
+    trial<DmmaCfg<64, 64, 32, 32, 3, 16, 3>>("cp_64x64_medium", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<32, 32, 16, 16, 3, 32, 1>>("cp_32x32_small", sh, A, B, C, Cref, d_cnt, false);
+    trial<DmmaCfg<16, 32, 16, 8, 8, 32, 1>>("cp_16x32_tiny_s8", sh, A, B, C, Cref, d_cnt, false);
+    trial_tma<moa::TmaMain>("64x64_s4_3cta", sh, A, B, C, Cref, d_cnt);
+    trial_tma<moa::TmaCfg<64, 128, 32, 32, 4, 2, 16>>("64x128_s4_2cta", sh, A, B, C, Cref, d_cnt);
     CK(cudaFree(A)); CK(cudaFree(B)); CK(cudaFree(C)); CK(cudaFree(Cref)); CK(cudaFree(d_cnt));
   }
   return 0;
