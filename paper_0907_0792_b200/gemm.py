@@ -75,22 +75,32 @@ def run_colmajor(params: GemmParams, a_cm: np.ndarray, b_cm: np.ndarray, c_cm: n
 
 def gemm_baseline(params: GemmParams, a: MoaArray, b: MoaArray, c: MoaArray, *,
                   workers: int = 1, backend: str | None = None) -> MoaArray:
-    """alpha*A*B + beta*C on row-major arrays; returns a new array (c unchanged)."""
+    """alpha*A*B + beta*C on row-major arrays; returns a new array (c unchanged).
+
+    Host operands take the same path as the MoA products (kernel.stage_host
+    in, pinned result out through kernel.d2h_split), and C is not read when
+    beta == 0 (as dgemm), so the harness compares like with like."""
     import torch
+
+    from .kernel import d2h_split, stage_host
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
     m, n, k = params.m, params.n, params.k
     for arr, shape, name in ((a, (m, k), "A"), (b, (k, n), "B"), (c, (m, n), "C")):
         if arr.shape != shape:
             raise ShapeError(f"{name}: expected shape {shape}, got {arr.shape}")
-    dev = torch.device("cuda")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f64 = np.dtype(np.float64)
 
     def dev2d(x: MoaArray, r: int, cc: int):
-        t = x.data if x.is_device else torch.from_numpy(np.array(x.data, dtype=np.float64))
-        return t.to(device=dev, dtype=torch.float64).view(r, cc)
+        t = x.data.to(device=dev, dtype=torch.float64) if x.is_device else stage_host(x.data, dev, f64)
+        return t.view(r, cc)
 
-    out = _device_gemm(params, dev2d(a, m, k), dev2d(b, k, n), dev2d(c, m, n))
+    c_dev = dev2d(c, m, n) if params.beta != 0.0 else None
+    out = _device_gemm(params, dev2d(a, m, k), dev2d(b, k, n), c_dev)
     flat = out.contiguous().view(-1)
     if a.is_device or b.is_device or c.is_device:
         return MoaArray._wrap((m, n), flat)
-    return MoaArray._wrap((m, n), flat.cpu().numpy())
+    host = torch.empty(flat.numel(), dtype=torch.float64, pin_memory=True)
+    d2h_split(host, flat, torch.cuda.current_stream(dev))
+    return MoaArray._wrap((m, n), host.numpy())
