@@ -18,7 +18,6 @@ count, like surplus reference workers, do nothing.  For one process per GPU
 
 from __future__ import annotations
 
-import numpy as np
 
 from . import _native
 from .arrays import MoaArray
