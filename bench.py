@@ -235,7 +235,11 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
     flush = L2Flusher(device)
     stream = torch.cuda.current_stream(device)
 
-    if world > 1:
+    # Strong-scaled jobs (c4/c5) broadcast B inside every step.  A weak-scaled
+    # job (c2) has B resident on every rank when the clock starts (broadcast
+    # once, below), so its step is the rank's own product with no collective.
+    bcast_in_step = world > 1 and SCALING[w.key] == "strong"
+    if bcast_in_step:
         from paper_0907_0792_b200.distributed import sharded_product
         gplan = job_plan(w, world)
         # strong-scaled (x,+) f64 products pipeline B's broadcast in k-chunks
@@ -249,19 +253,22 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
         def step():
             launch(sub, c_dev, a_dev, b_dev, w.ops)
 
+    if world > 1:
+        # B on every rank (the kernel-only leg below and weak-scaled steps read b_dev)
+        dist.broadcast(b_dev, src=0, group=group)
+        dist.barrier()
     for _ in range(warmup):
         step()
     torch.cuda.synchronize(device)
     if world > 1:
-        dist.broadcast(b_dev, src=0, group=group)  # the kernel-only leg below reads b_dev
         dist.barrier()
     torch.cuda.synchronize(device)
-    # Single GPU: the step is captured once into a CUDA graph, so each timed
-    # step is one graph launch and the events bracket device work only (no
-    # host-side launch gaps).  N>1 keeps eager steps (the broadcast inside may
-    # run over gloo, which cannot be captured).
+    # Steps without a collective are captured once into a CUDA graph, so each
+    # timed step is one graph launch and the events bracket device work only
+    # (no host-side launch gaps).  Steps with the broadcast inside stay eager
+    # (it may run over gloo, which cannot be captured).
     graph, per_step_launches = None, None
-    if world == 1:
+    if not bcast_in_step:
         l0 = _native.launch_count()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
@@ -308,7 +315,7 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
         flush()
         s.record(stream)
         if graph is not None:
-            graph.replay()  # at N=1 the step is exactly the product launch
+            graph.replay()  # a graph-captured step is exactly the product launch
         else:
             launch(sub, c_dev, a_dev, b_dev, w.ops)
         e.record(stream)
@@ -553,9 +560,11 @@ def main() -> None:
             "data": "synthetic (seeded generators of SURVEY.md §8d; no public dataset)",
             "config": {"workload": f"{w.key}: {w.description}", "M": m, "K": k, "N": n,
                        "rows_per_rank": rows_range[1] - rows_range[0],
-                       "parallelism": f"row-sharded x{world}, B broadcast ({dist.get_backend().upper()})"
-                       if world > 1
-                       else "single GPU",
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"row-sharded x{world}, B broadcast "
+                                       f"({dist.get_backend().upper()}) "
+                                       + ("inside every step" if scaling == "strong" else
+                                          "once, before the timed region")),
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "cuda_graph": bool(dev.get("graph"))},
             "e2e": {"value": round(e2e_value, 3), "unit": unit, "h2d_bytes_per_step": h2d,

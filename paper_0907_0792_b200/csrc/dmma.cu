@@ -285,9 +285,12 @@ cudaError_t launch_dmma(const Problem& p) {
   auto tiles = [&](int bm, int bn) { return ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn); };
   // TMA-staged 64x64 kernel (dmma_tma.cu) once it fills the SMs: 96.9% of the
   // DMMA peak at c4 vs 88.9% for the cp.async kernels
-  // (profiles/r01_tune_dmma_tma_cfgs.jsonl); below that the small cp.async
-  // tiles win (more CTAs)
-  if (tiles(64, 64) >= kNumSMs && dmma_tma_eligible(p)) return launch_dmma_tma(p);
+  // (profiles/r01_tune_dmma_tma_cfgs.jsonl); below that its 16x32-tile form
+  // (more CTAs; profiles/r01_tune_dmma_tiny.jsonl: at or below the cp.async
+  // tiny/small tiles on every shape tried)
+  if (dmma_tma_eligible(p))
+    return tiles(64, 64) >= kNumSMs ? launch_dmma_tma(p) : launch_dmma_tma_tiny(p);
+  // unaligned operands: per-thread cp.async tiles
   if (tiles(64, 128) >= 2 * kNumSMs) return dmma_dispatch<CfgLarge>(p);
   if (tiles(64, 64) >= kNumSMs) return dmma_dispatch<CfgMedium>(p);
   if (tiles(32, 32) >= kNumSMs) return dmma_dispatch<CfgSmall>(p);

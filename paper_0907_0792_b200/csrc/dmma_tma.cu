@@ -229,6 +229,133 @@ cudaError_t dmma_tma_launch(const Problem& p) {
   return cudaGetLastError();
 }
 
+// ---- tiny problems (fewer than one wave of 64x64 tiles, e.g. BASELINE c1) ----
+// 16 x 32 CTA tiles of four 16 x 8 warps: one DMMA chain per warp, the most
+// warps such a problem gives (one warp already saturates its sub-partition's
+// DMMA pipe, tools/mb_dmma_latency.cu).  The cp.async version of this tile
+// spends ~35 issue slots per DMMA on per-thread copy addressing and
+// bounds arithmetic with one warp per scheduler (ncu: 2209 instructions per
+// warp for 64 DMMAs, every slot ~4 cycles apart); here one thread issues two
+// TMA boxes per 32-deep slab and the warps only wait, load fragments and MMA.
+// No swizzle: the boxes are four doubles wider than the slab (A: 16 x 36,
+// B: 32 x 36 — the extra columns are the neighbouring slab/tile, or TMA's zero
+// fill, and are never read), so rows sit 288 bytes apart and every m16n8k4
+// fragment LDS.64 (A[g][k+t], B[k+t][g]) covers each bank once per half-warp.
+// Plain MMA rows/columns, k ascending in 4-wide DMMA steps from k = 0: the
+// bits equal every other K1 configuration.
+struct TinyCfg {
+  static constexpr int BM = 16, BN = 32, BK = 32, PAD = 4, WARPS = BN / 8, THREADS = 32 * WARPS;
+  static constexpr int A_PITCH = BK + PAD, B_PITCH = BN + PAD;  // doubles
+  static constexpr int A_BYTES = BM * A_PITCH * 8, B_BYTES = BK * B_PITCH * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static_assert(A_BYTES % 128 == 0 && STAGE_BYTES % 128 == 0, "TMA destinations 128-byte aligned");
+};
+
+template <int STAGES, bool ACC>
+__global__ void __launch_bounds__(TinyCfg::THREADS, 1)
+    dmma_tiny_tma_kernel(double* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
+                         int64_t tiles_n, const __grid_constant__ CUtensorMap map_a,
+                         const __grid_constant__ CUtensorMap map_b) {
+  using T = TinyCfg;
+  extern __shared__ __align__(128) unsigned char tt_raw[];
+  unsigned char* base = tt_raw + ((128u - (tma::smem_addr(tt_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * T::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int64_t m0 = (blockIdx.x / tiles_n) * T::BM, n0 = (blockIdx.x % tiles_n) * T::BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3, wn0 = 8 * warp;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], T::WARPS);
+    }
+    tma::mbar_init_fence();
+  }
+  __syncthreads();
+
+  const int64_t KT = (K + T::BK - 1) / T::BK;
+  auto issue = [&](int stage, int64_t kt) {  // one thread
+    unsigned char* st = base + stage * T::STAGE_BYTES;
+    mbar_expect_tx(&full[stage], T::STAGE_BYTES);
+    load_2d(st, &map_a, (int)(kt * T::BK), (int)m0, &full[stage]);
+    load_2d(st + T::A_BYTES, &map_b, (int)n0, (int)(kt * T::BK), &full[stage]);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; s++)
+      if (s < KT) issue(s, s);
+  }
+
+  double acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    if (ACC) {
+      const int64_t row = m0 + g + (q >> 1) * 8, col = n0 + wn0 + 2 * t + (q & 1);
+      acc[q] = (row < M && col < N) ? c[row * ldc + col] : 0.0;
+    } else {
+      acc[q] = 0.0;
+    }
+  }
+
+  for (int64_t kt = 0; kt < KT; kt++) {
+    const int stage = (int)(kt % STAGES);
+    mbar_wait(&full[stage], (unsigned)((kt / STAGES) & 1));
+    const double* as = reinterpret_cast<const double*>(base + stage * T::STAGE_BYTES);
+    const double* bs = reinterpret_cast<const double*>(base + stage * T::STAGE_BYTES + T::A_BYTES);
+    const double* a0p = as + g * T::A_PITCH + t;
+    const double* a1p = a0p + 8 * T::A_PITCH;
+    const double* bp = bs + t * T::B_PITCH + wn0 + g;
+#pragma unroll
+    for (int kk = 0; kk < T::BK; kk += 4)
+      dmma_step(acc, a0p[kk], a1p[kk], bp[kk * T::B_PITCH]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (tid == 0 && kt >= 1 && kt - 1 + STAGES < KT) {
+      const int ps = (int)((kt - 1) % STAGES);
+      mbar_wait(&empty[ps], (unsigned)(((kt - 1) / STAGES) & 1));
+      issue(ps, kt - 1 + STAGES);
+    }
+  }
+
+  const bool pair_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(c) % 16 == 0);
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int64_t row = m0 + g + 8 * h, col = n0 + wn0 + 2 * t;
+    if (row >= M) continue;
+    double* crow = c + row * ldc;
+    if (pair_ok && col + 1 < N) {
+      *reinterpret_cast<double2*>(crow + col) = make_double2(acc[2 * h], acc[2 * h + 1]);
+    } else {
+      if (col < N) crow[col] = acc[2 * h];
+      if (col + 1 < N) crow[col + 1] = acc[2 * h + 1];
+    }
+  }
+}
+
+// 8 stages keep a whole 256-deep K (c1) in flight
+template <int STAGES = 8>
+cudaError_t dmma_tiny_tma_launch(const Problem& p) {
+  using T = TinyCfg;
+  CUtensorMap map_a, map_b;
+  if (!make_tensor_map_2d(&map_a, p.a, 8, p.M, p.K, p.lda, T::BM, T::A_PITCH, false) ||
+      !make_tensor_map_2d(&map_b, p.b, 8, p.K, p.N, p.ldb, T::BK, T::B_PITCH, false))
+    return cudaErrorInvalidValue;
+  auto kern = p.accumulate ? dmma_tiny_tma_kernel<STAGES, true> : dmma_tiny_tma_kernel<STAGES, false>;
+  const size_t smem = (size_t)STAGES * T::STAGE_BYTES + 128 + 16 * STAGES;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles_m = (p.M + T::BM - 1) / T::BM, tiles_n = (p.N + T::BN - 1) / T::BN;
+  const int64_t tiles = tiles_m * tiles_n;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  kern<<<(unsigned)tiles, T::THREADS, smem, p.stream>>>(static_cast<double*>(p.c), p.M, p.N, p.K,
+                                                        p.ldc, tiles_n, map_a, map_b);
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool dmma_tma_eligible(const Problem& p) {
@@ -241,5 +368,13 @@ bool dmma_tma_eligible(const Problem& p) {
 }
 
 cudaError_t launch_dmma_tma(const Problem& p) { return dmma_tma_launch<TmaMain>(p); }
+
+// 8 stages (110 KB, whole K of c1 in flight) while the grid fits one CTA per
+// SM; beyond that 4 stages, so four CTAs share an SM
+// (profiles/r01_tune_dmma_tiny.jsonl: c1 8.2 vs 9.0 us; 1024x256x512 16.4 vs 20.5 us)
+cudaError_t launch_dmma_tma_tiny(const Problem& p) {
+  const int64_t tiles = ((p.M + TinyCfg::BM - 1) / TinyCfg::BM) * ((p.N + TinyCfg::BN - 1) / TinyCfg::BN);
+  return tiles <= kNumSMs ? dmma_tiny_tma_launch<8>(p) : dmma_tiny_tma_launch<4>(p);
+}
 
 }  // namespace moa

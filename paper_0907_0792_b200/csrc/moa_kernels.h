@@ -35,6 +35,8 @@ cudaError_t launch_dmma(const Problem& p);
 // the same product with TMA-staged operands (dmma_tma.cu); bitwise identical
 bool dmma_tma_eligible(const Problem& p);
 cudaError_t launch_dmma_tma(const Problem& p);
+// ... and its 16x32-tile form for problems below one wave of 64x64 tiles
+cudaError_t launch_dmma_tma_tiny(const Problem& p);
 // everything else: CUDA-core semiring kernel (exact compare-select fold, plus
 // the device-checked FMNMX3 fast loop for add/subtract x min/max).  semiring.cu
 cudaError_t launch_semiring(const Problem& p);

@@ -400,6 +400,36 @@ def test_dmma_tma_edges_bitwise_equal_cp_async_path(rng):
                   sum_tolerance(k, rows, b))
 
 
+@pytest.mark.parametrize("mkn", [(70, 610, 258),    # <= 148 16x32 tiles: 8-stage ring, refills
+                                 (600, 610, 300),   # > 148 tiles: 4-stage ring
+                                 (256, 256, 256)])  # BASELINE c1: whole K in flight
+def test_dmma_tiny_tma_bitwise_equal_cp_async_path(mkn, rng):
+    """Problems below one wave of 64x64 tiles take the 16x32-tile TMA kernel
+    when rows are 16-byte aligned and the cp.async tiles otherwise: same k
+    order, so bitwise equal, in write-only and accumulate mode, with ragged M/N
+    and K past the pipeline depth (ring refills)."""
+    torch = _torch()
+    m, k, n = mkn
+    a = rng.random(m * k + 1) * 2 - 1
+    b = rng.random(k * n) * 2 - 1
+    init = rng.random(m * n) * 2 - 1
+    bd = _dev(b)
+    aligned = _dev(np.ascontiguousarray(a[1:]))
+    shifted = _dev(a)[1:]  # 8-byte aligned A rows: TMA ineligible
+    plan = plan_inner((m, k), (k, n))
+    for acc in (False, True):
+        outs = []
+        for ad in (aligned, shifted):
+            c = _dev(init.copy())
+            launch(plan, c, ad, bd, moa.MUL_ADD, accumulate=acc)
+            outs.append(c.cpu().numpy())
+        assert_bits_equal(outs[0], outs[1], f"acc={acc}")
+        want = oracle.product(a[1:], b, m, k, n, MUL, ADD, res=init.copy() if acc else None)
+        tol = sum_tolerance(k, a, b) + (k + 1) * 2.0**-52 * float(np.max(np.abs(init)))
+        assert_within(outs[0], want, tol, f"acc={acc}")
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("dt,mkn", [(np.float32, (257, 131, 300)),   # odd K, unaligned: cp.async
                                     (np.float32, (1000, 132, 1004)),  # 16-byte rows: TMA kernel
                                     (np.float64, (257, 131, 300))])   # exact fold, specials
