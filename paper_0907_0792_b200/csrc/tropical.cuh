@@ -251,7 +251,7 @@ constexpr int TT_A_BYTES = TBM * TBK * 4, TT_B_BYTES = TBK * TBN * 4;  // 16 KiB
 constexpr int TT_STAGE_BYTES = TT_A_BYTES + TT_B_BYTES;
 constexpr size_t TT_SMEM = (size_t)TSTAGES * TT_STAGE_BYTES + 1024 + 64;
 
-template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1>
+template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false>
 __global__ void __launch_bounds__(TNT, MINB)
     tropical_tma_kernel(float* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                         const unsigned* special, int64_t tiles_m, int64_t tiles_n,
@@ -308,10 +308,23 @@ __global__ void __launch_bounds__(TNT, MINB)
                       4 * tx;
     const int64_t krem = K - kt * TBK;
     const int kend = krem < TBK ? (int)krem : TBK;
-    const int npairs = kend >> 1;
-#pragma unroll UNR
-    for (int kp = 0; kp < npairs; kp++) {
-      const int k = 2 * kp;
+    // k-pair (k, k+1) of row i with A values (a0, a1) and B rows k, k+1
+    auto fold_pair = [&](int i, float a0, float a1, const float4 (&b0)[2], const float4 (&b1)[2]) {
+#pragma unroll
+      for (int g = 0; g < 2; g++) {
+#pragma unroll
+        for (int p = 0; p < 2; p++) {
+          const float x0 = p ? b0[g].z : b0[g].x, x1 = p ? b0[g].w : b0[g].y;
+          const float y0 = p ? b1[g].z : b1[g].x, y1 = p ? b1[g].w : b1[g].y;
+          const unsigned long long s = pair_op_bcast<C>(x0, x1, a0);
+          const unsigned long long t = pair_op_bcast<C>(y0, y1, a1);
+          const int j = 4 * g + 2 * p;
+          acc[i][j] = fold3<R, INTFOLD>(acc[i][j], lo32(s), lo32(t));
+          acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], hi32(s), hi32(t));
+        }
+      }
+    };
+    auto kpair = [&](int k) {
       const int aoff = ((((k >> 2) ^ ty) & 7) << 4) + ((k & 3) << 2);
       float4 b0[2], b1[2];
 #pragma unroll
@@ -322,22 +335,44 @@ __global__ void __launch_bounds__(TNT, MINB)
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         const float2 av = *reinterpret_cast<const float2*>(as + i * 16 * 128 + aoff);
+        fold_pair(i, av.x, av.y, b0, b1);
+      }
+    };
+    int kdone = 0;
+    if constexpr (QUAD) {
+      // four k per step: B rows k..k+3 held in registers, one 16-byte A load
+      // (k..k+3 are one swizzle chunk) per row — 16 shared loads per 256
+      // (a, b) pairs instead of 24
+      const int nquads = kend >> 2;
+#pragma unroll 1
+      for (int kq = 0; kq < nquads; kq++) {
+        const int k = 4 * kq;
+        const int aoff = ((kq ^ ty) & 7) << 4;
+        float4 bq[4][2];
 #pragma unroll
-        for (int g = 0; g < 2; g++) {
+        for (int r = 0; r < 4; r++)
 #pragma unroll
-          for (int p = 0; p < 2; p++) {
-            const float x0 = p ? b0[g].z : b0[g].x, x1 = p ? b0[g].w : b0[g].y;
-            const float y0 = p ? b1[g].z : b1[g].x, y1 = p ? b1[g].w : b1[g].y;
-            const unsigned long long s = pair_op_bcast<C>(x0, x1, av.x);
-            const unsigned long long t = pair_op_bcast<C>(y0, y1, av.y);
-            const int j = 4 * g + 2 * p;
-            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], lo32(s), lo32(t));
-            acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], hi32(s), hi32(t));
-          }
+          for (int g = 0; g < 2; g++)
+            bq[r][g] = *reinterpret_cast<const float4*>(bs + (k + r) * TBN + 64 * g);
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const float4 av = *reinterpret_cast<const float4*>(as + i * 16 * 128 + aoff);
+          fold_pair(i, av.x, av.y, bq[0], bq[1]);
+          fold_pair(i, av.z, av.w, bq[2], bq[3]);
         }
       }
+      kdone = 4 * nquads;
+      if (kend - kdone >= 2) {
+        kpair(kdone);
+        kdone += 2;
+      }
+    } else {
+      const int npairs = kend >> 1;
+#pragma unroll UNR
+      for (int kp = 0; kp < npairs; kp++) kpair(2 * kp);
+      kdone = 2 * npairs;
     }
-    if (kend & 1) {  // lone last k: scalar combine + 2-input fold
+    if (kdone < kend) {  // lone last k: scalar combine + 2-input fold
       const int k = kend - 1;
       const int aoff = ((((k >> 2) ^ ty) & 7) << 4) + ((k & 3) << 2);
 #pragma unroll
@@ -389,13 +424,13 @@ inline bool tropical_tma_eligible(const Problem& p) {
          p.ldb < (int64_t(1) << 36) && tensor_maps_available();
 }
 
-template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1>
+template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false>
 cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
   CUtensorMap map_a, map_b;
   if (!make_tensor_map_2d(&map_a, p.a, 4, p.M, p.K, p.lda, TBM, TBK, true) ||
       !make_tensor_map_2d(&map_b, p.b, 4, p.K, p.N, p.ldb, TBK, TBN, false))
     return cudaErrorInvalidValue;
-  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR>;
+  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR, QUAD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT_SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
@@ -411,7 +446,14 @@ template <int C, int R, int MODE, bool ACC>
 cudaError_t tropical_launch(const Problem& p, const unsigned* special) {
   // TMA-staged kernel when the layout allows it: 19.5 vs 18.6 T pairs/s at c5
   // (profiles/r01_tune_tropical_tma.jsonl); bit-identical results
-  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE, ACC>(p, special);
+  // Four k per step (B rows in registers, 16-byte A loads) once the grid fills
+  // both CTA slots of every SM: 222.2 vs 228.7 ms at c5; on grids below that
+  // the shorter two-k step wins (profiles/r01_tune_tropical_quad.jsonl)
+  if (tropical_tma_eligible(p)) {
+    const int64_t tiles = ((p.M + TBM - 1) / TBM) * ((p.N + TBN - 1) / TBN);
+    return tiles >= 2 * kNumSMs ? tropical_tma_launch<C, R, MODE, ACC, 2, 1, true>(p, special)
+                                : tropical_tma_launch<C, R, MODE, ACC>(p, special);
+  }
   const bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);

@@ -575,6 +575,29 @@ def test_tropical_tma_strided_rows_odd_k(rng):
             assert not np.delete(got, np.s_[0::step], axis=0).any()
 
 
+@pytest.mark.parametrize("k", [70, 67])
+def test_tropical_quad_step_on_full_grids(k, rng):
+    """Grids of >= 296 128x128 tiles take the four-k step of the TMA tropical
+    kernel (tail: one k-pair and/or a lone k); every fast fold mode — unsigned
+    order (VIMNMX3), signed (FMNMX3), max-times (FMUL2) — bitwise vs the
+    reference and vs the exact loop."""
+    m, n = 2048, 2432
+    cases = (("add", "min", 0.0), ("subtract", "max", 50.0), ("multiply", "max", 0.0))
+    for comb, red, shift in cases:
+        ops = op_pair(comb, red)
+        c, r = ops.codes()
+        a = rng.random(m * k, dtype=np.float32) * np.float32(100) - np.float32(shift)
+        b = rng.random(k * n, dtype=np.float32) * np.float32(100)
+        if comb == "add":
+            a[rng.random(m * k) < 0.05] = np.inf
+        A = MoaArray((m, k), a, dtype=np.float32)
+        B = MoaArray((k, n), b, dtype=np.float32)
+        got = moa.inner(A, B, ops).data
+        want = oracle.product(a, b, m, k, n, c, r, workers=8).astype(np.float32)
+        assert_bits_equal(got, want, f"{ops} k={k}")
+        assert_bits_equal(moa.inner(A, B, ops, exact=True).data, want, f"{ops} k={k} exact")
+
+
 def _division_operands(rng, n, dt):
     """n dividends and n divisors spanning every exponent, mantissas of all
     ones, powers of two, the reciprocal path's range edges, zeros,
