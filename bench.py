@@ -242,9 +242,10 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
     if bcast_in_step:
         from paper_0907_0792_b200.distributed import sharded_product
         gplan = job_plan(w, world)
-        # strong-scaled (x,+) f64 products pipeline B's broadcast in k-chunks
-        chunks = 8 if (SCALING[w.key] == "strong" and w.ops.codes() == (2, 0)
-                       and w.dtype == np.float64) else 1
+        # strong-scaled jobs pipeline B's broadcast in k-chunks where the fold
+        # replays exactly under chunked accumulation ((x,+) f64, (add, min))
+        from paper_0907_0792_b200.distributed import bcast_chunk_align
+        chunks = 8 if bcast_chunk_align(w.ops, tdt) is not None else 1
 
         def step():
             sharded_product(gplan, a_dev, b_dev if rank == 0 else None, w.ops, group=group,

@@ -79,6 +79,27 @@ def k_chunks(K: int, chunks: int, align: int = 16) -> list[tuple[int, int]]:
     return [(k0, min(K, k0 + step)) for k0 in range(0, K, step)]
 
 
+# (combine, reduce) codes whose fold replays exactly when split into k-chunks
+# accumulated into C: min/max of sums or differences — the fold is one
+# compare-select chain either way, C holds the running value exactly (no
+# float32 rounding can move it: a nonzero sum of two floats never rounds to
+# zero, and rounding is monotone), and the fast tropical loops seed from C
+_CHUNKABLE_FOLDS = {(0, 2), (0, 3), (1, 2), (1, 3)}
+
+
+def bcast_chunk_align(ops: OpPair, dtype) -> int | None:
+    """k alignment of the chunks for a pipelined broadcast of B, or None when
+    chunked accumulation would not reproduce one pass bit for bit."""
+    torch = _torch()
+    codes = ops.codes()
+    if codes == (2, 0):
+        return 16 if dtype == torch.float64 else None  # the DMMA k-slab (f64 DMMA route only)
+    if codes in _CHUNKABLE_FOLDS and dtype in (torch.float32, torch.float64, torch.int32,
+                                               torch.int64):
+        return 32  # the tropical / semiring k-slab
+    return None
+
+
 def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, group=None,
                     src: int = 0, exact: bool = False, out=None,
                     row_kernel: Callable | None = None, bcast_chunks: int = 1):
@@ -89,11 +110,13 @@ def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, grou
     result block (rows r0..r1 of C) on the same device as a_block.
 
     ``bcast_chunks > 1`` pipelines the broadcast of B with the compute for
-    (multiply, add) on float64: B is broadcast in k-chunks (asynchronously, in
-    order) and the kernel for chunk i runs as soon as chunk i has arrived,
-    accumulating into C (MOA_FLAG_ACCUMULATE) while later chunks are still on
-    the wire.  Chunk boundaries are multiples of the DMMA k-slab, so the
-    result is bitwise identical to one pass.
+    (multiply, add) on float64 and for (add|subtract, min|max): B is broadcast
+    in k-chunks (asynchronously, in order) and the kernel for chunk i runs as
+    soon as chunk i has arrived, accumulating into C (MOA_FLAG_ACCUMULATE)
+    while later chunks are still on the wire.  Chunk boundaries are multiples
+    of the kernels' k-slab, and those folds replay exactly under chunked
+    accumulation (``bcast_chunk_align``), so the result is bitwise identical
+    to one pass; other pairs broadcast B whole.
     """
     torch, dist = _torch(), _dist()
     world, rank = dist.get_world_size(group), dist.get_rank(group)
@@ -104,8 +127,9 @@ def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, grou
                          f"A elements, got {a_block.numel()}")
     c = out if out is not None else torch.empty(sub.noproc * sub.elsinop,
                                                 dtype=a_block.dtype, device=a_block.device)
-    pipelined = (bcast_chunks > 1 and row_kernel is None and not exact
-                 and ops.codes() == (2, 0) and a_block.dtype == torch.float64)
+    align = bcast_chunk_align(ops, a_block.dtype)
+    pipelined = (bcast_chunks > 1 and row_kernel is None and align is not None
+                 and not (exact and ops.codes() == (2, 0)))
     if not pipelined:
         b_all = broadcast_operand(b, plan, src=src, group=group, device=a_block.device,
                                   dtype=a_block.dtype)
@@ -119,7 +143,7 @@ def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, grou
         b_all = b.reshape(-1).to(a_block.device).contiguous()
     else:
         b_all = torch.empty(k * n, dtype=a_block.dtype, device=a_block.device)
-    chunks = k_chunks(k, bcast_chunks)
+    chunks = k_chunks(k, bcast_chunks, align)
     works = [dist.broadcast(b_all[k0 * n:k1 * n], src=src, group=group, async_op=True)
              for k0, k1 in chunks]
     for i, ((k0, k1), work) in enumerate(zip(chunks, works)):
@@ -127,7 +151,7 @@ def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, grou
         if sub.noproc:
             part = KernelPlan(plan.mode, sub.noproc, k1 - k0, n, plan.lstride, plan.rstride,
                               plan.restride, plan.result_shape)
-            launch(part, c, a_block[k0:], b_all[k0 * n:], ops, accumulate=i > 0)
+            launch(part, c, a_block[k0:], b_all[k0 * n:], ops, exact=exact, accumulate=i > 0)
     return c
 
 

@@ -82,3 +82,24 @@ def test_sharded_product_gloo(world, mode):
         results.append(q.get())
     assert all(p.exitcode == 0 for p in procs), results
     assert ("ok", True) in results, results
+
+
+def test_bcast_chunk_alignment_only_for_replayable_folds():
+    """Pipelined broadcasts of B are offered only where chunked accumulation
+    replays one pass bit for bit: (x,+) on float64 (DMMA k-slab 16) and
+    (add|subtract, min|max) on every dtype (k-slab 32)."""
+    import torch
+
+    import paper_0907_0792_b200 as moa
+    from paper_0907_0792_b200.distributed import bcast_chunk_align, k_chunks
+    assert bcast_chunk_align(moa.MUL_ADD, torch.float64) == 16
+    assert bcast_chunk_align(moa.MUL_ADD, torch.float32) is None
+    for comb in ("add", "subtract"):
+        for red in ("min", "max"):
+            for dt in (torch.float32, torch.float64, torch.int32, torch.int64):
+                assert bcast_chunk_align(moa.op_pair(comb, red), dt) == 32
+    for comb, red in (("add", "add"), ("multiply", "min"), ("divide", "max"), ("min", "min")):
+        assert bcast_chunk_align(moa.op_pair(comb, red), torch.float32) is None
+    chunks = k_chunks(16384, 8, 32)
+    assert chunks[0] == (0, 2048) and chunks[-1] == (14336, 16384)
+    assert all(k0 % 32 == 0 for k0, _ in chunks)

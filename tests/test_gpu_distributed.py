@@ -56,6 +56,35 @@ def _worker(rank, world, port, q):
         if rank == 0:
             ref = moa.inner(moa.MoaArray((m, k), a), moa.MoaArray((k, n), b)).data
             ok &= bool(torch.equal(full.view(-1), ref.view(-1)))
+        # ... and for (add|subtract, min|max), fast folds and the exact loop
+        # (NaN / -0 / negative data), float32 and int32: same bits
+        m, k, n = 300, 203, 388
+        for ops, dt, poison in ((moa.op_pair("add", "min"), torch.float32, None),
+                                (moa.op_pair("subtract", "max"), torch.float32, "negative"),
+                                (moa.op_pair("add", "max"), torch.float32, "nan"),
+                                (moa.op_pair("add", "min"), torch.float64, "negzero"),
+                                (moa.op_pair("subtract", "min"), torch.int32, None)):
+            av = rng.random(m * k) * 100
+            bv = rng.random(k * n) * 100
+            av[rng.random(m * k) < 0.05] = np.inf if dt.is_floating_point else 7
+            if poison == "negative":
+                av -= 50
+            elif poison == "nan":
+                av[rng.random(m * k) < 0.01] = np.nan
+            elif poison == "negzero":
+                av[rng.random(m * k) < 0.05] = -0.0
+                bv[rng.random(k * n) < 0.05] = -0.0
+            a = torch.from_numpy(av).to(dt).cuda()
+            b = torch.from_numpy(bv).to(dt).cuda()
+            plan = moa.plan_inner((m, k), (k, n))
+            r0, r1 = row_block(m, world, rank)
+            blk = sharded_product(plan, a[r0 * k:r1 * k], b if rank == 0 else None, ops,
+                                  bcast_chunks=3)
+            full = gather_rows(blk, plan)
+            if rank == 0:
+                ref = moa.inner(moa.MoaArray((m, k), a), moa.MoaArray((k, n), b), ops).data
+                same = torch.equal(full.view(-1).view(torch.uint8), ref.view(-1).view(torch.uint8))
+                ok &= bool(same)
         # the host-buffer form used by bench.py's e2e leg
         from paper_0907_0792_b200.distributed import sharded_product_host
         m, k, n = 100, 64, 96
