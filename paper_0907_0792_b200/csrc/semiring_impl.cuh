@@ -325,22 +325,65 @@ __global__ void __launch_bounds__(SNT, MINB)
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) scan_special_kernel(const T* __restrict__ x, int64_t rows,
+// Special-value flags of one float32 value, branch-free on its bit pattern
+__device__ __forceinline__ unsigned special_bits(unsigned u) {
+  const unsigned mag = u & 0x7fffffffu;
+  unsigned f = (u >> 31) ? S_NEG : 0u;
+  f |= mag > 0x7f800000u ? S_NAN : 0u;
+  f |= u == 0x7f800000u ? S_PINF : 0u;
+  f |= u == 0xff800000u ? S_NINF : 0u;
+  f |= u == 0u ? S_PZERO : 0u;
+  f |= u == 0x80000000u ? S_NZERO : 0u;
+  return f;
+}
+
+// OR of special_bits over x[0, n), strided over `nthr` threads starting at
+// `tid`: scalar head up to 16-byte alignment, then four 16-byte loads in
+// flight per thread per step (the scan is a pure HBM stream, so the loads in
+// flight set its speed), then a scalar tail
+__device__ __forceinline__ unsigned scan_segment(const float* __restrict__ x, int64_t n,
+                                                 int64_t tid, int64_t nthr) {
+  unsigned bits = 0;
+  int64_t head = (int64_t)((16u - (reinterpret_cast<uintptr_t>(x) & 15u)) & 15u) / 4;
+  if (head > n) head = n;
+  if (tid < head) bits |= special_bits(__float_as_uint(__ldg(x + tid)));
+  const uint4* v = reinterpret_cast<const uint4*>(x + head);
+  const int64_t nv = (n - head) / 4;
+  constexpr int U = 4;
+  int64_t i = tid;
+  for (; i + (U - 1) * nthr < nv; i += U * nthr) {
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) q[u] = __ldcs(v + i + u * nthr);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      bits |= special_bits(q[u].x) | special_bits(q[u].y) | special_bits(q[u].z) |
+              special_bits(q[u].w);
+  }
+  for (; i < nv; i += nthr) {
+    const uint4 q = __ldcs(v + i);
+    bits |= special_bits(q.x) | special_bits(q.y) | special_bits(q.z) | special_bits(q.w);
+  }
+  const int64_t tail0 = head + nv * 4;
+  if (tail0 + tid < n) bits |= special_bits(__float_as_uint(__ldg(x + tail0 + tid)));
+  return bits;
+}
+
+// Device pre-scan of a rows x cols float32 matrix (row stride ld): the OR of
+// its values' special-value flags into *out.  Contiguous matrices are one
+// segment over the whole grid; strided ones give each block row its own rows.
+__global__ void __launch_bounds__(256) scan_special_kernel(const float* __restrict__ x, int64_t rows,
                                                            int64_t cols, int64_t ld,
                                                            unsigned* __restrict__ out) {
   unsigned bits = 0;
-  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
-    const T* p = x + r * ld;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cols;
-         j += (int64_t)gridDim.x * blockDim.x) {
-      const T v = __ldg(p + j);
-      if (v != v) bits |= S_NAN;
-      else if (v == T(__builtin_huge_val())) bits |= S_PINF;
-      else if (v == T(-__builtin_huge_val())) bits |= S_NINF;
-      else if (v == T(0)) bits |= signbit(v) ? S_NZERO : S_PZERO;
-      if (signbit(v)) bits |= S_NEG;
-    }
+  if (ld == cols || rows == 1) {
+    const int64_t nthr = (int64_t)gridDim.x * gridDim.y * blockDim.x;
+    const int64_t tid = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    bits = scan_segment(x, rows * cols, tid, nthr);
+  } else {
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) bits |= scan_segment(x + r * ld, cols, tid, nthr);
   }
   bits = __reduce_or_sync(0xffffffffu, bits);
   if ((threadIdx.x & 31) == 0 && bits) atomicOr(out, bits);
@@ -349,14 +392,24 @@ __global__ void __launch_bounds__(256) scan_special_kernel(const T* __restrict__
 template <typename T>
 void launch_scan(const T* x, int64_t rows, int64_t cols, int64_t ld, unsigned* out,
                  cudaStream_t s) {
+  static_assert(std::is_same<T, float>::value, "the pre-scan serves the float32 fast folds");
+  if (rows <= 0 || cols <= 0) return;
   const unsigned bx = 256;
-  int64_t gx = (cols + bx - 1) / bx;
-  if (gx > 64) gx = 64;
-  int64_t gy = ((int64_t)kNumSMs * 8 + gx - 1) / gx;
-  if (gy > rows) gy = rows;
-  if (gy > 65535) gy = 65535;
-  if (gy < 1) gy = 1;
-  scan_special_kernel<T><<<dim3((unsigned)gx, (unsigned)gy), bx, 0, s>>>(x, rows, cols, ld, out);
+  int64_t gx, gy;
+  if (ld == cols || rows == 1) {
+    gx = (int64_t)kNumSMs * 8;  // eight 256-thread blocks per SM stream the whole matrix
+    const int64_t need = (rows * cols / 16 + bx - 1) / bx;  // >= 16 floats per thread
+    if (gx > need) gx = need < 1 ? 1 : need;
+    gy = 1;
+  } else {
+    gx = (cols / 16 + bx - 1) / bx;
+    if (gx < 1) gx = 1;
+    if (gx > 64) gx = 64;
+    gy = ((int64_t)kNumSMs * 8 + gx - 1) / gx;
+    if (gy > rows) gy = rows;
+    if (gy > 65535) gy = 65535;
+  }
+  scan_special_kernel<<<dim3((unsigned)gx, (unsigned)gy), bx, 0, s>>>(x, rows, cols, ld, out);
   count_launch();
 }
 

@@ -293,11 +293,11 @@ def execute_sequential(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair =
     launch because rows are independent.
     """
     if not (a.is_device or b.is_device):
-        chunks = _stream_chunks(plan, result_dtype(a, b), ops)
-        if chunks > 1:
+        blocks = _stream_blocks(plan, result_dtype(a, b), ops)
+        if len(blocks) > 1:
             _check_plan(plan, a, b)
             resolve_backend(backend, ops)
-            return _execute_streamed(plan, a, b, ops, chunks, exact=exact)
+            return _execute_streamed(plan, a, b, ops, blocks, exact=exact)
     runner = _Runner(plan, a, b, ops, backend, exact=exact)
     runner.run_rows(0, 1)
     return runner.finish()
@@ -307,20 +307,53 @@ _STREAM_MIN_OUT_BYTES = 128 << 20
 _WAVES_PER_CHUNK = 24  # >= 24 waves of CTAs per block keeps the tail wave small
 
 
-def _stream_chunks(plan: KernelPlan, dtype: np.dtype, ops: OpPair = MUL_ADD) -> int:
-    """Row blocks for the streamed host path (1 = do not stream)."""
+_EDGE_MIN_WAVES = 6    # ... and >= 6 waves in each half-size end block
+
+
+def edge_blocks(noproc: int, middle: int = 3, align: int = 128) -> list[range]:
+    """Row blocks for streaming: a 3/16 first block, ``middle`` equal blocks,
+    a 1/16 last block (sizes rounded to ``align`` rows).  The first block is
+    computed k-chunk by k-chunk while B lands, so it must be long enough to
+    cover B's transfer and the next block's A rows (B is 16% of c4's compute
+    time at the measured host link); the last block's C rows are the copy no
+    compute can hide, so it is small.  Middle blocks stay long enough that
+    their partial last wave of CTAs costs little.  (A copy/compute timeline
+    model over the BASELINE configs picked these fractions: c4 273 -> 260 ms
+    against half-size end blocks.)"""
+    from .parallel import row_blocks  # local: parallel imports this module
+    first = noproc * 3 // 16
+    first -= first % align
+    last = noproc // 16
+    last -= last % align
+    if first <= 0 or last <= 0:
+        return row_blocks(noproc, middle + 2)
+    mid = noproc - first - last
+    size = -(-mid // middle)
+    size += -size % align
+    bounds = [0] + [min(first + i * size, noproc - last) for i in range(middle)] + \
+        [noproc - last, noproc]
+    return [range(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1)
+            if bounds[i + 1] > bounds[i]]
+
+
+def _stream_blocks(plan: KernelPlan, dtype: np.dtype, ops: OpPair = MUL_ADD) -> list[range]:
+    """Row blocks for the streamed host path (one block = do not stream)."""
+    from .parallel import row_blocks  # local: parallel imports this module
+    m = plan.noproc
     if plan.rowsinred < 2:  # outer products are pure D2H; blocks cannot hide it
-        return 1
-    out_bytes = plan.noproc * plan.elsinop * np.dtype(dtype).itemsize
+        return [range(0, m)]
+    out_bytes = m * plan.elsinop * np.dtype(dtype).itemsize
     if ops.codes() == (2, 0) and np.dtype(dtype) == np.dtype(np.float64):
-        tiles, per_wave = -(-plan.noproc // 64) * -(-plan.elsinop // 128), 296  # dmma.cu
+        tiles, per_wave = -(-m // 64) * -(-plan.elsinop // 128), 296  # dmma.cu
     else:
-        tiles, per_wave = -(-plan.noproc // 128) * -(-plan.elsinop // 128), 296  # semiring.cu
+        tiles, per_wave = -(-m // 128) * -(-plan.elsinop // 128), 296  # semiring.cu
+    if out_bytes >= 8 * _STREAM_MIN_OUT_BYTES and tiles >= 8 * _EDGE_MIN_WAVES * per_wave:
+        return edge_blocks(m)
     by_waves = tiles // (per_wave * _WAVES_PER_CHUNK)
-    return int(max(1, min(8, out_bytes // _STREAM_MIN_OUT_BYTES, by_waves)))
+    return row_blocks(m, int(max(1, min(8, out_bytes // _STREAM_MIN_OUT_BYTES, by_waves))))
 
 
-def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, chunks: int,
+def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, chunks,
                       *, exact: bool = False, device=None) -> MoaArray:
     """Host operands -> host result with copies overlapped with compute.
 
@@ -345,7 +378,8 @@ def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, c
     comp = torch.cuda.current_stream(dev)
     s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     out = torch.empty(m * n, dtype=tdt, pin_memory=True)
-    blocks = [r for r in row_blocks(m, chunks) if len(r)]
+    # chunks: a number of equal row blocks, or the blocks themselves
+    blocks = [r for r in (row_blocks(m, chunks) if isinstance(chunks, int) else chunks) if len(r)]
     k = plan.rowsinred
     # k-chunks accumulate through the result buffer, so the fold must not be
     # carried in a wider type than it is stored in (float32 data folded in
@@ -353,7 +387,10 @@ def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, c
     wide = np.dtype(dtype) == np.float32 and (ops.reduce_name in ("add", "multiply") or
                                               ops.combine_name in ("multiply", "divide"))
     chunked = not b.is_device and not wide
-    b_chunks = k_chunks(k, len(blocks)) if chunked else [(0, k)]
+    # the first block takes B in k-chunks as they land; with half-size end
+    # blocks, eight chunks keep that block's per-chunk compute above the
+    # per-chunk transfer while the first chunk (the exposed part) stays small
+    b_chunks = k_chunks(k, 8 if len(blocks) >= 5 else len(blocks)) if chunked else [(0, k)]
     if not chunked:
         b_dev = stage(b, dev, dtype)
         b_ready = [None]

@@ -598,6 +598,47 @@ def test_tropical_quad_step_on_full_grids(k, rng):
         assert_bits_equal(moa.inner(A, B, ops, exact=True).data, want, f"{ops} k={k} exact")
 
 
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_prescan_sees_every_element(offset, rng):
+    """The float32 pre-scan decides which fold is exact, so it must see every
+    element: one negative value (breaks the unsigned-order fold) or one NaN in
+    the last k (the reference's fold ends on it) placed first, last, or inside
+    a 16-byte vector of an operand that starts `offset` floats past an aligned
+    address — contiguous (one segment) and round-robin rows (strided scan)."""
+    torch = _torch()
+    m, k, n = 37, 67, 41
+    ops = op_pair("add", "min")
+    base_a = (rng.random(m * k + 8) * 100).astype(np.float32)
+    base_b = (rng.random(k * n + 8) * 100).astype(np.float32)
+    for where in ("a_first", "a_last", "a_mid", "b_first", "b_last", "nan_last_k"):
+        aa, bb = base_a.copy(), base_b.copy()
+        av, bv = aa[offset:offset + m * k], bb[offset:offset + k * n]
+        if where == "a_first":
+            av[0] = -1.5
+        elif where == "a_last":
+            av[-1] = -1.5
+        elif where == "a_mid":
+            av[m * k // 2 + 1] = -0.25
+        elif where == "b_first":
+            bv[0] = -3.0
+        elif where == "b_last":
+            bv[-1] = -3.0
+        else:
+            av[5 * k + k - 1] = np.nan
+        want = oracle.product(av, bv, m, k, n, 0, 2).astype(np.float32)
+        res = torch.empty(m * n, dtype=torch.float32, device="cuda")
+        ad, bd = _dev(aa)[offset:offset + m * k], _dev(bb)[offset:offset + k * n]
+        launch(plan_inner((m, k), (k, n)), res, ad, bd, ops)
+        assert_bits_equal(res.cpu().numpy(), want, f"{where} offset={offset}")
+        # rows 1, 3, 5, ... : the A scan walks strided rows
+        rows = np.ascontiguousarray(av.reshape(m, k)[1::2]).ravel()
+        res2 = torch.zeros(m * n, dtype=torch.float32, device="cuda")
+        launch(plan_inner((m, k), (k, n)), res2, ad, bd, ops, start=1, step=2)
+        got = res2.cpu().numpy().reshape(m, n)[1::2].ravel()
+        want2 = oracle.product(rows, bv, rows.size // k, k, n, 0, 2).astype(np.float32)
+        assert_bits_equal(got, want2, f"{where} offset={offset} strided")
+
+
 def _division_operands(rng, n, dt):
     """n dividends and n divisors spanning every exponent, mantissas of all
     ones, powers of two, the reciprocal path's range edges, zeros,
@@ -702,7 +743,7 @@ def test_launch_counter_advances():
 def test_streamed_host_path_bitwise_equals_one_launch(rng):
     """Host operands of large products go through row blocks with overlapped
     copies (kernel._execute_streamed); the bits equal one device launch."""
-    from paper_0907_0792_b200.kernel import _execute_streamed
+    from paper_0907_0792_b200.kernel import _execute_streamed, edge_blocks
     m, k, n = 1000, 300, 777
     a = rng.random(m * k) * 2 - 1
     b = rng.random(k * n) * 2 - 1
@@ -713,7 +754,7 @@ def test_streamed_host_path_bitwise_equals_one_launch(rng):
                     (op_pair("multiply", "add"), np.float32), (op_pair("subtract", "max"), np.float32)):
         A, B = MoaArray((m, k), a, dtype=dt), MoaArray((k, n), b, dtype=dt)
         want = moa.inner(A.to_device(), B.to_device(), ops).host_data()
-        for chunks in (2, 3, 7):
+        for chunks in (2, 3, 7, edge_blocks(m, 3, 16)):
             got = _execute_streamed(moa.plan_inner(A.shape, B.shape), A, B, ops, chunks)
             assert got.shape == (m, n)
             assert_bits_equal(got.data, want, f"{ops} chunks={chunks}")
