@@ -268,15 +268,24 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
     # timed step is one graph launch and the events bracket device work only
     # (no host-side launch gaps).  Steps with the broadcast inside stay eager
     # (it may run over gloo, which cannot be captured).
+    # Under torchrun the NCCL watchdog thread keeps querying events, so the
+    # capture is thread-local there; should it still fail, the steps stay eager.
     graph, per_step_launches = None, None
     if not bcast_in_step:
         l0 = _native.launch_count()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step()
-        per_step_launches = _native.launch_count() - l0
-        graph.replay()
-        torch.cuda.synchronize(device)
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, capture_error_mode="thread_local" if world > 1
+                                  else "global"):
+                step()
+            per_step_launches = _native.launch_count() - l0
+            graph.replay()
+            torch.cuda.synchronize(device)
+        except RuntimeError as exc:  # pragma: no cover - depends on the driver/NCCL
+            print(f"[bench] rank {rank}: CUDA graph capture failed ({exc}); eager steps",
+                  file=sys.stderr)
+            graph, per_step_launches = None, None
+            torch.cuda.synchronize(device)
     run_step = graph.replay if graph is not None else step
     launches0 = _native.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -390,11 +399,16 @@ def measure_e2e(w, rows_range, a_pin, b_pin, steps, warmup, device, world, rank,
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
+    marks = []
     for _ in range(steps):
         out = None
         out = step()
+        marks.append(time.perf_counter())
     torch.cuda.synchronize(device)
     elapsed = time.perf_counter() - t0
+    if os.environ.get("MOA_BENCH_VERBOSE"):
+        per = [round((b_ - a_) * 1e3, 2) for a_, b_ in zip([t0] + marks[:-1], marks)]
+        print(f"[bench] {w.key} e2e per-step ms: {per}", file=sys.stderr)
     if world > 1:
         t = torch.tensor([elapsed], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -487,6 +501,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-inner", action="store_true", help="skip the extra inner-product legs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--legs", nargs="*", default=None,
+                    help="inner-product legs to run beside c2 (default: all of c1 c3 c4 c5)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo only to exercise the "
                          "multi-rank code path on fewer GPUs than ranks; timings meaningless)")
@@ -579,7 +595,7 @@ def main() -> None:
 
     if world == 1 and not args.no_inner and w.key == "c2":
         inner = {}
-        for key in ("c1", "c3", "c4", "c5"):
+        for key in [k for k in ("c1", "c3", "c4", "c5") if args.legs is None or k in args.legs]:
             wi = WORKLOADS[key]
             ai, bi = wi.generate()
             mi = wi.mkn[0]
@@ -591,6 +607,19 @@ def main() -> None:
                           "kernel_ms": round(d["kernel_ms_mean"], 4),
                           "roofline": roofline(wi, mi, d["kernel_ms_mean"]),
                           "clocks": d["clocks"]}
+            # the same product end to end through moa.inner on pinned host
+            # arrays (H2D of A and B, the product, D2H of C inside the clock)
+            ap, bp = pinned_copy(ai), pinned_copy(bi)
+            e2e_st = 20 if key == "c1" else 3
+            el_i = measure_e2e(wi, (0, mi), ap, bp, e2e_st, 3, device, 1, 0)
+            isz_i = np.dtype(wi.dtype).itemsize
+            ki, ni = wi.mkn[1], wi.mkn[2]
+            inner[key]["e2e"] = {"value": round(to_unit(wi, amt * e2e_st, el_i), 2),
+                                 "unit": METRIC[key][1], "ms_per_step": round(el_i / e2e_st * 1e3, 3),
+                                 "h2d_bytes_per_step": (mi * ki + ki * ni) * isz_i,
+                                 "d2h_bytes_per_step": mi * ni * isz_i,
+                                 "path": "moa.inner on pinned host MoaArrays (streamed row blocks)"}
+            del ap, bp
             if rank == 0 and not args.no_cpu:
                 # the reference's own loop on a small row sample (~1-3 s of CPU)
                 rows_i = {"c1": mi, "c3": 1024, "c4": 32, "c5": 32}[key]
