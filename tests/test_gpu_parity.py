@@ -766,20 +766,28 @@ def test_kernels_never_write_outside_their_rows(rng):
     and between the owned rows stay untouched."""
     torch = _torch()
     sentinel = -12345.678
-    cases = [((70, 33, 45), op_pair("multiply", "add")), ((70, 33, 45), op_pair("add", "min")),
-             ((70, 1, 257), op_pair("multiply", "add")), ((70, 0, 45), op_pair("add", "max")),
-             ((129, 20, 131), op_pair("divide", "multiply")), ((5, 40, 2048), op_pair("min", "max"))]
-    for (m, k, n), ops in cases:
+    # (start, step) 1, 3: odd row strides (cp.async routes); 0, 2 with even K:
+    # 16-byte aligned rows, so the TMA kernels (16x32 / 64x64 DMMA, tropical) run
+    cases = [((70, 33, 45), op_pair("multiply", "add"), 1, 3),
+             ((70, 33, 45), op_pair("add", "min"), 1, 3),
+             ((70, 1, 257), op_pair("multiply", "add"), 1, 3),
+             ((70, 0, 45), op_pair("add", "max"), 1, 3),
+             ((129, 20, 131), op_pair("divide", "multiply"), 1, 3),
+             ((5, 40, 2048), op_pair("min", "max"), 1, 3),
+             ((70, 34, 46), op_pair("multiply", "add"), 0, 2),
+             ((4000, 36, 2370), op_pair("multiply", "add"), 0, 2),
+             ((300, 40, 260), op_pair("add", "min"), 0, 2)]
+    for (m, k, n), ops, start, step in cases:
         for dt in (torch.float64, torch.float32):
             a = _dev(rng.random(m * k) * 2 - 1, dt)
             b = _dev(rng.random(k * n) * 2 - 1, dt)
             plan = plan_inner((m, k), (k, n))
             pad = 37
             buf = torch.full((m * n + 2 * pad,), sentinel, dtype=dt, device="cuda")
-            launch(plan, buf[pad:pad + m * n], a, b, ops, start=1, step=3)
+            launch(plan, buf[pad:pad + m * n], a, b, ops, start=start, step=step)
             host = buf.cpu().numpy()
             want_sent = np.ones(m * n + 2 * pad, dtype=bool)
-            for i in range(1, m, 3):
+            for i in range(start, m, step):
                 want_sent[pad + i * n:pad + (i + 1) * n] = False
             got_sent = host == np.array(sentinel, dtype=host.dtype)
             assert np.array_equal(got_sent[want_sent], np.ones(want_sent.sum(), bool)), \
