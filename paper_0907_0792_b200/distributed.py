@@ -19,7 +19,7 @@ from __future__ import annotations
 
 from typing import Callable
 
-from .kernel import KernelPlan, launch
+from .kernel import KernelPlan, d2h_split, launch
 from .ops import MUL_ADD, OpPair
 
 
@@ -184,8 +184,7 @@ def sharded_product_host(plan: KernelPlan, a_block_host, b_host, ops: OpPair = M
     b_dev = _to_device(b_host, device) if b_host is not None else None
     c = sharded_product(plan, a_dev, b_dev, ops, group=group, src=src, exact=exact)
     out = torch.empty(c.numel(), dtype=c.dtype, pin_memory=True)
-    out.copy_(c, non_blocking=True)
-    torch.cuda.current_stream(c.device).synchronize()
+    d2h_split(out, c, torch.cuda.current_stream(c.device))
     return out.numpy()
 
 
