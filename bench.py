@@ -18,9 +18,12 @@ A step is one pass of the product over one unit of synthetic input:
   between timed steps (a 256 MiB write, outside the events); each step is
   bracketed by CUDA events on the launching stream; sum over steps, max over
   ranks.
-* ``e2e``: the public API with pinned HOST buffers — H2D of A and B, kernel,
-  D2H of the whole result — per step (``outer``/``inner`` at N=1,
-  ``distributed.sharded_product_host`` at N>1).
+* ``e2e``: the reference-facing C ABI with HOST buffers — one
+  ``moa_product_rows_host`` call per step on page-locked A, B and result (H2D
+  of A and B, the product, D2H of the whole result, all inside the clock) at
+  N=1; ``distributed.sharded_product_host`` at N>1.  ``e2e_api`` is the same
+  through the public Python API (``moa.outer``/``moa.inner`` on pinned host
+  MoaArrays).
 Multi-GPU (torchrun): the outer product scales weakly (each rank owns one
 unit of 65,536 result rows; B broadcast from rank 0), the large inner products
 strongly (result rows of one 16384^3 product split across ranks).
@@ -417,6 +420,27 @@ def measure_e2e(w, rows_range, a_pin, b_pin, steps, warmup, device, world, rank,
     return elapsed
 
 
+def measure_e2e_cabi(w, a_pin, b_pin, steps, warmup, device):
+    """The reference-facing boundary with host buffers: one
+    moa_product_rows_host call (include/moa_b200.h) per step on page-locked A,
+    B and result; returns seconds for ``steps`` calls."""
+    import torch
+
+    from paper_0907_0792_b200.kernel import launch_host
+    plan = plan_for(w)
+    m, k, n = w.mkn
+    res = torch.empty(m * n, dtype=a_pin.dtype, pin_memory=True).numpy()
+    a, b = a_pin.numpy(), b_pin.numpy()
+    for _ in range(warmup):
+        launch_host(plan, res, a, b, w.ops, device=device.index)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        launch_host(plan, res, a, b, w.ops, device=device.index)
+    elapsed = time.perf_counter() - t0
+    del res
+    return elapsed
+
+
 # ---------------------------------------------------------------------------- CPU legs
 def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 500, rows: int | None = None,
                        min_reps: int = 3):
@@ -567,6 +591,12 @@ def main() -> None:
         h2d = (m * k + k * n) * isz
         d2h = m * n * isz
     e2e_value = to_unit(w, job_amount * e2e_steps, el)
+    e2e_api = None
+    if world == 1:  # headline e2e through the C ABI; the public API beside it
+        e2e_api = {"value": round(e2e_value, 3), "unit": METRIC[w.key][1],
+                   "path": "moa.outer/inner on pinned host MoaArrays"}
+        el = measure_e2e_cabi(w, a_pin, b_pin, e2e_steps, 2, device)
+        e2e_value = to_unit(w, job_amount * e2e_steps, el)
     del a_pin, b_pin
 
     metric, unit = METRIC[w.key]
@@ -586,9 +616,10 @@ def main() -> None:
                        "cuda_graph": bool(dev.get("graph"))},
             "e2e": {"value": round(e2e_value, 3), "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "path": "moa.outer/inner on pinned host MoaArrays" if world == 1 else
-                    "distributed.sharded_product_host"},
+                    "path": "moa_product_rows_host (C ABI) on page-locked host buffers"
+                    if world == 1 else "distributed.sharded_product_host"},
             "gpu_launches": launches,
+            **({"e2e_api": e2e_api} if e2e_api else {}),
             "roofline": roofline(w, rows_range[1] - rows_range[0], kern_ms),
             "kernel_ms": round(kern_ms, 4),
             "clocks": dev["clocks"]}
@@ -614,11 +645,17 @@ def main() -> None:
             el_i = measure_e2e(wi, (0, mi), ap, bp, e2e_st, 3, device, 1, 0)
             isz_i = np.dtype(wi.dtype).itemsize
             ki, ni = wi.mkn[1], wi.mkn[2]
-            inner[key]["e2e"] = {"value": round(to_unit(wi, amt * e2e_st, el_i), 2),
-                                 "unit": METRIC[key][1], "ms_per_step": round(el_i / e2e_st * 1e3, 3),
+            el_c = measure_e2e_cabi(wi, ap, bp, e2e_st, 3, device)
+            inner[key]["e2e"] = {"value": round(to_unit(wi, amt * e2e_st, el_c), 2),
+                                 "unit": METRIC[key][1], "ms_per_step": round(el_c / e2e_st * 1e3, 3),
                                  "h2d_bytes_per_step": (mi * ki + ki * ni) * isz_i,
                                  "d2h_bytes_per_step": mi * ni * isz_i,
-                                 "path": "moa.inner on pinned host MoaArrays (streamed row blocks)"}
+                                 "path": "moa_product_rows_host (C ABI) on page-locked host "
+                                         "buffers (streamed row blocks)"}
+            inner[key]["e2e_api"] = {"value": round(to_unit(wi, amt * e2e_st, el_i), 2),
+                                     "unit": METRIC[key][1],
+                                     "ms_per_step": round(el_i / e2e_st * 1e3, 3),
+                                     "path": "moa.inner on pinned host MoaArrays (streamed row blocks)"}
             del ap, bp
             if rank == 0 and not args.no_cpu:
                 # the reference's own loop on a small row sample (~1-3 s of CPU)

@@ -100,6 +100,28 @@ int moa_product_rows(int dtype, void* res, const void* a, const void* b,
                      int64_t start, int64_t step,
                      uint32_t flags, void* stream);
 
+/*
+ * The same product with HOST buffers — the exact drop-in for
+ * _ckernel.product_rows, whose res/a/b are host numpy arrays
+ * (_ckernel.pyx:75-88): identical arguments and semantics to
+ * moa_product_rows, with res/a/b in host memory and the CUDA device index in
+ * place of the stream.  Copies the row set's A rows (packed by 2-D copies),
+ * B, and with MOA_FLAG_ACCUMULATE the row set's res rows to the device, runs
+ * the product, and writes back exactly res's rows start, start+step, ... (so
+ * concurrent calls on disjoint row sets of one res are safe, as in the
+ * reference's execute_parallel, parallel.py:26-43).  Large products are
+ * streamed in row blocks with copies overlapping the kernels (page-locked host
+ * buffers overlap fully; pageable ones are staged by the driver).  Blocks
+ * until res holds the result.  MOA_E_BOUNDS also when the row set's result
+ * rows would overlap (restride*step < elsinop).
+ */
+int moa_product_rows_host(int dtype, void* res, const void* a, const void* b,
+                          int64_t noproc, int64_t rowsinred, int64_t elsinop,
+                          int64_t lstride, int64_t rstride, int64_t restride,
+                          int combine_code, int reduce_code,
+                          int64_t start, int64_t step,
+                          uint32_t flags, int device);
+
 /* Message for the last failing call on this thread ("" if none). */
 const char* moa_last_error(void);
 

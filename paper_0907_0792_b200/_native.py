@@ -23,7 +23,7 @@ FLAG_ACCUMULATE = 1
 FLAG_EXACT = 2
 
 # every symbol include/moa_b200.h declares
-EXPORTS = ("moa_product_rows", "moa_last_error", "moa_abi_version",
+EXPORTS = ("moa_product_rows", "moa_product_rows_host", "moa_last_error", "moa_abi_version",
            "moa_launch_count", "moa_plan_kernel")
 
 _lock = threading.Lock()
@@ -39,6 +39,11 @@ def _bind(lib: ctypes.CDLL) -> None:
         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
         _i64, _i64, _i64, _i64, _i64, _i64,
         ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_uint32, ctypes.c_void_p]
+    lib.moa_product_rows_host.restype = ctypes.c_int
+    lib.moa_product_rows_host.argtypes = [
+        ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+        _i64, _i64, _i64, _i64, _i64, _i64,
+        ctypes.c_int, ctypes.c_int, _i64, _i64, ctypes.c_uint32, ctypes.c_int]
     lib.moa_last_error.restype = ctypes.c_char_p
     lib.moa_last_error.argtypes = []
     lib.moa_abi_version.restype = ctypes.c_int
@@ -66,7 +71,11 @@ def load() -> ctypes.CDLL:
             except OSError as exc:  # pragma: no cover - depends on the host
                 _load_error = f"cannot load {LIB_PATH}: {exc}"
                 raise BackendError(_load_error) from exc
-            _bind(lib)
+            try:
+                _bind(lib)
+            except AttributeError as exc:  # a stale build missing a newer entry point
+                _load_error = f"{LIB_PATH} is out of date ({exc}); rebuild it"
+                raise BackendError(_load_error) from exc
             _lib = lib
     return _lib
 
@@ -92,6 +101,22 @@ def product_rows(dtype: int, res_ptr: int, a_ptr: int, b_ptr: int,
     if rc != 0:
         msg = lib.moa_last_error().decode(errors="replace")
         raise BackendError(f"moa_product_rows failed ({rc}): {msg}")
+
+
+def product_rows_host(dtype: int, res_ptr: int, a_ptr: int, b_ptr: int,
+                      noproc: int, rowsinred: int, elsinop: int,
+                      lstride: int, rstride: int, restride: int,
+                      combine_code: int, reduce_code: int, start: int, step: int,
+                      flags: int, device: int) -> None:
+    """moa_product_rows_host on raw HOST pointers (blocks until res is written);
+    raises BackendError on failure."""
+    lib = load()
+    rc = lib.moa_product_rows_host(dtype, res_ptr, a_ptr, b_ptr, noproc, rowsinred, elsinop,
+                                   lstride, rstride, restride, combine_code, reduce_code,
+                                   start, step, flags, device)
+    if rc != 0:
+        msg = lib.moa_last_error().decode(errors="replace")
+        raise BackendError(f"moa_product_rows_host failed ({rc}): {msg}")
 
 
 def plan_kernel(dtype: int, noproc: int, rowsinred: int, elsinop: int,

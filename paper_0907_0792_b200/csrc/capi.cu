@@ -17,13 +17,16 @@
 #include "moa_kernels.h"
 #include "../../include/moa_b200.h"
 
+namespace {
+thread_local std::string t_last_error;
+}
+
 namespace moa {
 std::atomic<uint64_t> g_launches{0};
+void set_last_error(const std::string& msg) { t_last_error = msg; }
 }
 
 namespace {
-
-thread_local std::string t_last_error;
 
 int fail(int code, const std::string& msg) {
   t_last_error = msg;
@@ -109,6 +112,9 @@ int moa_product_rows(int dtype, void* res, const void* a, const void* b, int64_t
   p.accumulate = (flags & MOA_FLAG_ACCUMULATE) != 0;
   p.stream = static_cast<cudaStream_t>(stream);
 
+  // the launchers check cudaGetLastError(); drop a stale, non-sticky error an
+  // earlier call of this library left in this thread's runtime state
+  (void)cudaGetLastError();
   cudaError_t e = cudaSuccess;
   switch (r) {
     case Route::Fill: e = moa::launch_fill(p); break;

@@ -222,6 +222,42 @@ def _check_extents(plan: KernelPlan, res, a_dev, b_dev, start: int, step: int) -
             raise ValueError(f"{name} holds {have[name]} elements; the plan addresses {n}")
 
 
+def launch_host(plan: KernelPlan, res: np.ndarray, a: np.ndarray, b: np.ndarray, ops: OpPair,
+                *, start: int = 0, step: int = 1, exact: bool = False,
+                accumulate: bool = False, device: int | None = None) -> None:
+    """One moa_product_rows_host call on flat HOST numpy buffers — the
+    reference's ``product_rows(res, a, b, ...)`` contract (_ckernel.pyx:75-88)
+    with the product on ``device``.  Writes rows start::step of ``res`` (folds
+    into them with ``accumulate``) and returns when they hold the result."""
+    if not (res.dtype == a.dtype == b.dtype):
+        raise TypeError("operands and result must share one dtype")
+    for name, x in (("res", res), ("a", a), ("b", b)):
+        if x.ndim != 1 or not x.flags.c_contiguous:
+            raise ValueError(f"{name} must be a flat contiguous array")
+    if not res.flags.writeable:
+        raise ValueError("res must be writeable")
+    codes = ops.codes()
+    if codes is None:
+        raise ValueError("custom OpPair callables have no device implementation")
+    if step >= 1 and 0 <= start < plan.noproc and plan.elsinop:
+        last = start + (plan.noproc - 1 - start) // step * step
+        need = {"res": last * plan.restride + plan.elsinop}
+        if plan.rowsinred:
+            need["a"] = last * plan.lstride + plan.rowsinred
+            need["b"] = (plan.rowsinred - 1) * plan.rstride + plan.elsinop
+        for name, n in need.items():
+            have = {"res": res, "a": a, "b": b}[name].size
+            if have < n:
+                raise ValueError(f"{name} holds {have} elements; the plan addresses {n}")
+    if device is None:
+        device = _torch().cuda.current_device()
+    flags = (_native.FLAG_EXACT if exact else 0) | (_native.FLAG_ACCUMULATE if accumulate else 0)
+    _native.product_rows_host(native_dtype(res.dtype), res.ctypes.data, a.ctypes.data,
+                              b.ctypes.data, plan.noproc, plan.rowsinred, plan.elsinop,
+                              plan.lstride, plan.rstride, plan.restride, codes[0], codes[1],
+                              start, step, flags, int(device))
+
+
 class _Runner:
     """One planned product on one GPU, ready to run row sets into one result."""
 

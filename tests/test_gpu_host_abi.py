@@ -1,0 +1,177 @@
+"""moa_product_rows_host — the host-buffer form of the boundary (the exact
+drop-in for _ckernel.product_rows, _ckernel.pyx:75-88): against the
+device-pointer entry point on the same data (bitwise) and the CPU oracle,
+for every dtype, row sets start::step, accumulate mode, padded and
+overlapping strides, pageable and page-locked buffers, the streamed (row
+block) schedule, and its argument errors."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_0907_0792_b200 as moa
+from paper_0907_0792_b200 import op_pair
+from paper_0907_0792_b200.errors import BackendError
+from paper_0907_0792_b200.kernel import KernelPlan, launch, launch_host, plan_inner, plan_outer
+from parity import assert_bits_equal, assert_within, sum_tolerance
+
+pytestmark = pytest.mark.gpu
+
+DTYPES = (np.float64, np.float32, np.int32, np.int64)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _operands(rng, n, dt):
+    if np.dtype(dt).kind == "i":
+        return rng.integers(-50, 50, n).astype(dt)
+    return (rng.random(n) * 4 - 1).astype(dt)
+
+
+def _device_result(plan, res0, a, b, ops, **kw):
+    torch = _torch()
+    res = torch.from_numpy(res0.copy()).cuda()
+    launch(plan, res, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), ops, **kw)
+    return res.cpu().numpy()
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+def test_host_entry_equals_device_entry(dt, rng):
+    """Same bits as moa_product_rows on device copies of the same buffers, for
+    row sets start::step, write-only and accumulate, across op pairs."""
+    m, k, n = 77, 45, 66
+    a, b = _operands(rng, m * k, dt), _operands(rng, k * n, dt)
+    plan = plan_inner((m, k), (k, n))
+    pairs = [op_pair("multiply", "add"), op_pair("add", "min"), op_pair("subtract", "max"),
+             op_pair("max", "multiply"), op_pair("divide", "min")]
+    for ops in pairs:
+        for start, step in ((0, 1), (1, 3), (5, 2), (76, 4)):
+            for acc in (False, True):
+                res0 = _operands(rng, m * n, dt)
+                want = _device_result(plan, res0, a, b, ops, start=start, step=step, accumulate=acc)
+                got = res0.copy()
+                launch_host(plan, got, a, b, ops, start=start, step=step, accumulate=acc)
+                assert_bits_equal(got, want, f"{dt.__name__} {ops} {start}::{step} acc={acc}")
+
+
+def test_host_entry_matches_oracle_and_touches_only_its_rows(rng):
+    m, k, n = 60, 33, 47
+    a, b = rng.random(m * k) * 2 - 1, rng.random(k * n) * 2 - 1
+    plan = plan_inner((m, k), (k, n))
+    sentinel = -7.25
+    res = np.full(m * n, sentinel)
+    launch_host(plan, res, a, b, op_pair("add", "max"), start=2, step=5)
+    want = oracle.product(a, b, m, k, n, 0, 3).reshape(m, n)
+    got = res.reshape(m, n)
+    rows = np.arange(2, m, 5)
+    assert_bits_equal(got[rows].ravel(), want[rows].ravel())
+    others = np.setdiff1d(np.arange(m), rows)
+    assert np.all(got[others] == sentinel)
+    # (multiply, add) on the tensor cores: within the north-star tolerance
+    res = np.empty(m * n)
+    launch_host(plan, res, a, b, moa.MUL_ADD)
+    assert_within(res, oracle.product(a, b, m, k, n, 2, 0), sum_tolerance(k, a, b))
+
+
+def test_host_entry_padded_and_overlapping_strides(rng):
+    """lstride > K (padded A rows), rstride > N (padded B rows) and a row set
+    whose A rows overlap (lstride*step < K: the span path)."""
+    m, k, n = 40, 24, 30
+    ops = op_pair("add", "min")
+    # padded A rows (lstride = 31) and B rows (rstride = 37); C rows restride 35
+    lstride, rstride, restride = 31, 37, 35
+    a = rng.random(m * lstride)
+    b = rng.random(k * rstride)
+    plan = KernelPlan("inner", m, k, n, lstride, rstride, restride, (m, n))
+    res0 = np.full(m * restride, 3.5)
+    want = _device_result(plan, res0, a, b, ops, start=1, step=2)
+    got = res0.copy()
+    launch_host(plan, got, a, b, ops, start=1, step=2)
+    assert_bits_equal(got, want, "padded")
+    # overlapping A rows: lstride 10 < K = 24 (rows share elements)
+    plan = KernelPlan("inner", m, k, n, 10, n, n, (m, n))
+    a = rng.random((m - 1) * 10 + k)
+    b = rng.random(k * n)
+    res0 = np.zeros(m * n)
+    want = _device_result(plan, res0, a, b, ops)
+    got = res0.copy()
+    launch_host(plan, got, a, b, ops)
+    assert_bits_equal(got, want, "overlapping A rows")
+
+
+def test_host_entry_outer_fill_and_page_locked_buffers(rng):
+    torch = _torch()
+    x, y = rng.random(300) * 2 - 1, rng.random(513) * 2 - 1
+    res = np.empty(300 * 513)
+    launch_host(plan_outer((300,), (513,)), res, x, y, moa.MUL_ADD)
+    assert_bits_equal(res, (np.multiply.outer(x, y) + 0.0).ravel())
+    # K = 0: the identity everywhere (write-only), nothing under accumulate
+    res = np.full(6, 9.0)
+    launch_host(plan_inner((2, 0), (0, 3)), res, np.empty(0), np.empty(0), op_pair("add", "min"))
+    assert np.all(res == np.inf)
+    res = np.full(6, 9.0)
+    launch_host(plan_inner((2, 0), (0, 3)), res, np.empty(0), np.empty(0), op_pair("add", "min"),
+                accumulate=True)
+    assert np.all(res == 9.0)
+    # page-locked host buffers (the overlapped path) give the same bits
+    m, k, n = 90, 64, 128
+    a, b = rng.random(m * k), rng.random(k * n)
+    pa = torch.empty(m * k, dtype=torch.float64, pin_memory=True).numpy()
+    pb = torch.empty(k * n, dtype=torch.float64, pin_memory=True).numpy()
+    pr = torch.empty(m * n, dtype=torch.float64, pin_memory=True).numpy()
+    pa[:], pb[:] = a, b
+    plan = plan_inner((m, k), (k, n))
+    launch_host(plan, pr, pa, pb, op_pair("multiply", "max"))
+    assert_bits_equal(pr, oracle.product(a, b, m, k, n, 2, 3))
+
+
+@pytest.mark.parametrize("dt,ops", [(np.float64, moa.MUL_ADD),
+                                    (np.float32, op_pair("add", "min")),
+                                    (np.float32, op_pair("multiply", "add"))])
+def test_host_entry_streamed_blocks_equal_one_launch(dt, ops, rng):
+    """Results of >= 1 GiB run the streamed schedule (3/16 first block computed
+    per k-chunk of B, middle blocks, 1/16 last block; float32 sums take B
+    whole): bitwise equal to one device launch."""
+    torch = _torch()
+    esz = np.dtype(dt).itemsize
+    m, k, n = (8192, 96, 16384) if esz == 8 else (16384, 96, 16384)
+    a = (rng.random(m * k) * 100).astype(dt)
+    b = (rng.random(k * n) * 100).astype(dt)
+    plan = plan_inner((m, k), (k, n))
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    want = torch.empty(m * n, dtype=ad.dtype, device="cuda")
+    launch(plan, want, ad, bd, ops)
+    want = want.cpu().numpy()
+    del ad, bd
+    res = torch.empty(m * n, dtype=torch.from_numpy(a[:1]).dtype, pin_memory=True).numpy()
+    launch_host(plan, res, a, b, ops)
+    assert_bits_equal(res, want, f"{dt.__name__} {ops}")
+    # and with accumulate (res prefilled with the identity, as the reference does)
+    res[:] = ops.reduce_identity
+    launch_host(plan, res, a, b, ops, accumulate=True)
+    assert_bits_equal(res, want, f"{dt.__name__} {ops} accumulate")
+
+
+def test_host_entry_argument_errors(rng):
+    from paper_0907_0792_b200 import _native
+    a, b, res = np.zeros(12), np.zeros(12), np.zeros(9)
+    with pytest.raises(BackendError, match="step"):
+        _native.product_rows_host(0, res.ctypes.data, a.ctypes.data, b.ctypes.data,
+                                  3, 4, 3, 4, 3, 3, 2, 0, 0, 0, 0, 0)
+    with pytest.raises(BackendError, match="dtype"):
+        _native.product_rows_host(9, res.ctypes.data, a.ctypes.data, b.ctypes.data,
+                                  3, 4, 3, 4, 3, 3, 2, 0, 0, 1, 0, 0)
+    with pytest.raises(BackendError, match="overlap"):
+        _native.product_rows_host(0, res.ctypes.data, a.ctypes.data, b.ctypes.data,
+                                  3, 4, 3, 4, 3, 1, 2, 0, 0, 1, 0, 0)
+    with pytest.raises(BackendError, match="cudaSetDevice"):
+        _native.product_rows_host(0, res.ctypes.data, a.ctypes.data, b.ctypes.data,
+                                  3, 4, 3, 4, 3, 3, 2, 0, 0, 1, 0, 99)
+    # surplus worker / empty rows: no work, no error
+    _native.product_rows_host(0, res.ctypes.data, a.ctypes.data, b.ctypes.data,
+                              3, 4, 3, 4, 3, 3, 2, 0, 5, 1, 0, 0)

@@ -30,12 +30,16 @@ def _module():
 
 
 def test_backend_module_binds_the_abi():
-    """CPU-side: the module loads the library and binds moa_product_rows with
-    the reference's 13 arguments plus dtype, flags and stream."""
+    """CPU-side: the module loads the library (no torch) and binds the
+    host-buffer entry point with the reference's 13 arguments plus dtype,
+    flags and device (and the device-pointer one with a stream)."""
     mod = _module()
+    assert len(mod._lib.moa_product_rows_host.argtypes) == 16
     assert len(mod._lib.moa_product_rows.argtypes) == 16
     assert mod.MOA_FLAG_ACCUMULATE == 1
     assert callable(mod.product_rows)
+    src = (ROOT / "integration" / "moaprod_b200kernel.py").read_text()
+    assert "import torch" not in src
 
 
 @pytest.mark.gpu
