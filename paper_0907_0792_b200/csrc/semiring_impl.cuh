@@ -147,17 +147,25 @@ __global__ void __launch_bounds__(SNT, MINB)
 
   // ---- accumulators: rows ty*TM+i, columns col_of(j) ----
   A acc[TM][TN];
+  {
+    // Under ACCUMULATE the seeds come from C through opaque copies of its
+    // origin: otherwise the compiler keeps these addresses and bounds tests
+    // alive through the main loop for the epilogue and spills them.
+    int64_t om0 = m0, on0 = n0;
+    const T* oc = c;
+    if (ACC) asm volatile("" : "+l"(om0), "+l"(on0), "+l"(oc));
 #pragma unroll
-  for (int i = 0; i < TM; i++)
+    for (int i = 0; i < TM; i++)
 #pragma unroll
-    for (int j = 0; j < TN; j++) {
-      const int64_t row = m0 + ty * TM + i;
-      const int64_t col = n0 + col_of(j);
-      if (ACC && row < M && col < N)
-        acc[i][j] = A(c[row * ldc + col]);
-      else
-        acc[i][j] = ReduceOp<R>::template identity<A>();
-    }
+      for (int j = 0; j < TN; j++) {
+        const int64_t row = om0 + ty * TM + i;
+        const int64_t col = on0 + col_of(j);
+        if (ACC && row < M && col < N)
+          acc[i][j] = A(oc[row * ldc + col]);
+        else
+          acc[i][j] = ReduceOp<R>::template identity<A>();
+      }
+  }
   // ---- element-wise async copies into the k-pair layouts (zero-filled outside) ----
   // Per-thread bases are fixed for the whole kernel; a stage only adds k0.
   const int a_kk = tid % BK, a_r = tid / BK;

@@ -73,6 +73,9 @@ __device__ __forceinline__ void init_acc(float (&acc)[8][8], const float* c, int
                                          int64_t ldc, int64_t m0, int64_t n0, int r0, int rstep,
                                          int tx) {
   const float init = (INTFOLD && R == R_MAX) ? 0.0f : ReduceOp<R>::template identity<float>();
+  // opaque copies of C's origin: otherwise the compiler keeps these addresses
+  // and bounds tests alive through the main loop for the epilogue and spills
+  if (ACC) asm volatile("" : "+l"(m0), "+l"(n0), "+l"(c));
 #pragma unroll
   for (int i = 0; i < 8; i++)
 #pragma unroll

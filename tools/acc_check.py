@@ -15,7 +15,11 @@ n = 4096
 g = np.random.default_rng(0)
 plan = plan_inner((n, n), (n, n))
 cases = [(np.float32, "add", "min"), (np.float32, "add", "max"), (np.float64, "add", "min"),
-         (np.float64, "multiply", "add"), (np.float64, "multiply", "max"), (np.float64, "divide", "add")]
+         (np.float64, "multiply", "add"), (np.float64, "multiply", "max"), (np.float64, "divide", "add"),
+         (np.float64, "max", "max"), (np.float64, "min", "min"), (np.float64, "divide", "max"),
+         (np.float64, "max", "add"), (np.float64, "multiply", "multiply")]
+if len(sys.argv) > 1:  # only float64 routes
+    cases = [c for c in cases if c[0] == np.float64]
 for dt, comb, red in cases:
     a = torch.from_numpy((g.random(n * n) * 100).astype(dt)).cuda()
     b = torch.from_numpy((g.random(n * n) * 100 + 1).astype(dt)).cuda()
