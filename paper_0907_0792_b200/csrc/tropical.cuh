@@ -3,10 +3,12 @@
 // only), reduce in {min, max} — in their own kernels.
 //
 // Two kernels share the loop: tropical_tma_kernel (16-byte aligned rows:
-// TMA-staged tiles, mbarrier pipeline, no block barrier in the main loop) and
+// TMA-staged tiles, mbarrier pipeline, no block barrier in the main loop; 64x128
+// C tiles of 128 threads, three CTAs per SM, four k per step) and
 // tropical_kernel (any alignment: cp.async into padded A[BM][BK+4],
-// B[BK][BN+4]).  Operands stay in their natural row-major layouts; a thread
-// owns 8 rows and columns 64g + 4tx + c (g < 2, c < 4) of a 128x128 C tile.
+// B[BK][BN+4]; 128x128 tiles).  Operands stay in their natural row-major
+// layouts; a thread owns 8 rows and columns 64g + 4tx + c (g < 2, c < 4) of
+// its C tile.
 // For each k-pair (k, k+1) it forms, per row i and
 // column pair (j, j+1),
 //     s  = FADD2((B[k][j],   B[k][j+1]),   a[i][k]   broadcast)
@@ -250,22 +252,34 @@ __global__ void __launch_bounds__(TNT, 2)
 // Thread (ty, tx) owns rows ty + 16i (i < 8), so the two A rows a warp reads
 // per load differ in (r & 7) and sit in different banks, and the swizzle term
 // ((k>>2) ^ ty) & 7 is the same for all eight rows.
-constexpr int TT_A_BYTES = TBM * TBK * 4, TT_B_BYTES = TBK * TBN * 4;  // 16 KiB each
-constexpr int TT_STAGE_BYTES = TT_A_BYTES + TT_B_BYTES;
-constexpr size_t TT_SMEM = (size_t)TSTAGES * TT_STAGE_BYTES + 1024 + 64;
+// (BMT = 64: 64 x 128 CTA tiles of 128 threads, rows ty + 8i, three CTAs per
+// SM with up to 168 registers per thread instead of 128.)
+template <int BMT>
+struct TropTma {
+  static constexpr int BM = BMT, THREADS = 2 * BMT, ROW_STEP = BMT / 8;
+  static constexpr int A_BYTES = BMT * TBK * 4, B_BYTES = TBK * TBN * 4;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = (size_t)TSTAGES * STAGE_BYTES + 1024 + 64;
+  static_assert(ROW_STEP % 8 == 0, "rows ty + ROW_STEP*i keep the swizzle term ty & 7");
+};
+constexpr int TT_A_BYTES = TropTma<128>::A_BYTES, TT_B_BYTES = TropTma<128>::B_BYTES;
+constexpr int TT_STAGE_BYTES = TropTma<128>::STAGE_BYTES;
+constexpr size_t TT_SMEM = TropTma<128>::SMEM;
 
-template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false>
-__global__ void __launch_bounds__(TNT, MINB)
+template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false,
+          int BMT = 128>
+__global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
     tropical_tma_kernel(float* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                         const unsigned* special, int64_t tiles_m, int64_t tiles_n,
                         const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b) {
   static_assert(MODE == 1 || MODE == 2, "fast modes only");
+  using TT = TropTma<BMT>;
   constexpr bool INTFOLD = MODE == 2;
   if (tropical_mode_of<ACC>(C, special) != MODE) return;
   extern __shared__ __align__(16) unsigned char tt_raw[];
   unsigned char* base = tma::align1k(tt_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + TSTAGES * TT_STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + TSTAGES * TT::STAGE_BYTES);
   uint64_t* empty = full + TSTAGES;
 
   const int64_t pid = blockIdx.x;
@@ -273,7 +287,7 @@ __global__ void __launch_bounds__(TNT, MINB)
   const int64_t width = GM * tiles_n;
   const int64_t first_m = (pid / width) * GM;
   const int64_t gsize = (tiles_m - first_m) < GM ? (tiles_m - first_m) : GM;
-  const int64_t m0 = (first_m + (pid % width) % gsize) * TBM;
+  const int64_t m0 = (first_m + (pid % width) % gsize) * TT::BM;
   const int64_t n0 = ((pid % width) / gsize) * TBN;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15, lane = tid & 31;
 
@@ -281,7 +295,7 @@ __global__ void __launch_bounds__(TNT, MINB)
 #pragma unroll
     for (int s = 0; s < TSTAGES; s++) {
       tma::mbar_init(&full[s], 1);
-      tma::mbar_init(&empty[s], TNT / 32);
+      tma::mbar_init(&empty[s], TT::THREADS / 32);
     }
     tma::mbar_init_fence();
   }
@@ -289,10 +303,10 @@ __global__ void __launch_bounds__(TNT, MINB)
 
   const int64_t KT = (K + TBK - 1) / TBK;
   auto issue = [&](int stage, int64_t kt) {  // thread 0 only
-    unsigned char* st = base + stage * TT_STAGE_BYTES;
-    tma::mbar_expect_tx(&full[stage], TT_STAGE_BYTES);
+    unsigned char* st = base + stage * TT::STAGE_BYTES;
+    tma::mbar_expect_tx(&full[stage], TT::STAGE_BYTES);
     tma::load_2d(st, &map_a, (int)(kt * TBK), (int)m0, &full[stage]);
-    tma::load_2d(st + TT_A_BYTES, &map_b, (int)n0, (int)(kt * TBK), &full[stage]);
+    tma::load_2d(st + TT::A_BYTES, &map_b, (int)n0, (int)(kt * TBK), &full[stage]);
   };
   if (tid == 0) {
 #pragma unroll
@@ -301,13 +315,13 @@ __global__ void __launch_bounds__(TNT, MINB)
   }
 
   float acc[8][8];
-  init_acc<R, INTFOLD, ACC>(acc, c, M, N, ldc, m0, n0, ty, 16, tx);
+  init_acc<R, INTFOLD, ACC>(acc, c, M, N, ldc, m0, n0, ty, TT::ROW_STEP, tx);
 
   for (int64_t kt = 0; kt < KT; kt++) {
     const int stage = (int)(kt % TSTAGES);
     tma::mbar_wait(&full[stage], (unsigned)((kt / TSTAGES) & 1));
-    const unsigned char* as = base + stage * TT_STAGE_BYTES + ty * 128;
-    const float* bs = reinterpret_cast<const float*>(base + stage * TT_STAGE_BYTES + TT_A_BYTES) +
+    const unsigned char* as = base + stage * TT::STAGE_BYTES + ty * 128;
+    const float* bs = reinterpret_cast<const float*>(base + stage * TT::STAGE_BYTES + TT::A_BYTES) +
                       4 * tx;
     const int64_t krem = K - kt * TBK;
     const int kend = krem < TBK ? (int)krem : TBK;
@@ -337,7 +351,7 @@ __global__ void __launch_bounds__(TNT, MINB)
       }
 #pragma unroll
       for (int i = 0; i < 8; i++) {
-        const float2 av = *reinterpret_cast<const float2*>(as + i * 16 * 128 + aoff);
+        const float2 av = *reinterpret_cast<const float2*>(as + i * TT::ROW_STEP * 128 + aoff);
         fold_pair(i, av.x, av.y, b0, b1);
       }
     };
@@ -359,7 +373,7 @@ __global__ void __launch_bounds__(TNT, MINB)
             bq[r][g] = *reinterpret_cast<const float4*>(bs + (k + r) * TBN + 64 * g);
 #pragma unroll
         for (int i = 0; i < 8; i++) {
-          const float4 av = *reinterpret_cast<const float4*>(as + i * 16 * 128 + aoff);
+          const float4 av = *reinterpret_cast<const float4*>(as + i * TT::ROW_STEP * 128 + aoff);
           fold_pair(i, av.x, av.y, bq[0], bq[1]);
           fold_pair(i, av.z, av.w, bq[2], bq[3]);
         }
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(TNT, MINB)
       const int aoff = ((((k >> 2) ^ ty) & 7) << 4) + ((k & 3) << 2);
 #pragma unroll
       for (int i = 0; i < 8; i++) {
-        const float av = *reinterpret_cast<const float*>(as + i * 16 * 128 + aoff);
+        const float av = *reinterpret_cast<const float*>(as + i * TT::ROW_STEP * 128 + aoff);
 #pragma unroll
         for (int g = 0; g < 2; g++)
 #pragma unroll
@@ -402,7 +416,7 @@ __global__ void __launch_bounds__(TNT, MINB)
   const bool vec_store = (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(c) % 16 == 0);
 #pragma unroll
   for (int i = 0; i < 8; i++) {
-    const int64_t row = m0 + ty + 16 * i;
+    const int64_t row = m0 + ty + TT::ROW_STEP * i;
     if (row >= M) continue;
 #pragma unroll
     for (int g = 0; g < 2; g++) {
@@ -427,36 +441,37 @@ inline bool tropical_tma_eligible(const Problem& p) {
          p.ldb < (int64_t(1) << 36) && tensor_maps_available();
 }
 
-template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false>
+template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false,
+          int BMT = 128>
 cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
+  using TT = TropTma<BMT>;
   CUtensorMap map_a, map_b;
-  if (!make_tensor_map_2d(&map_a, p.a, 4, p.M, p.K, p.lda, TBM, TBK, true) ||
+  if (!make_tensor_map_2d(&map_a, p.a, 4, p.M, p.K, p.lda, TT::BM, TBK, true) ||
       !make_tensor_map_2d(&map_b, p.b, 4, p.K, p.N, p.ldb, TBK, TBN, false))
     return cudaErrorInvalidValue;
-  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR, QUAD>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT_SMEM);
+  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR, QUAD, BMT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT::SMEM);
   if (e != cudaSuccess) return e;
-  const int64_t tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
+  const int64_t tiles_m = (p.M + TT::BM - 1) / TT::BM, tiles_n = (p.N + TBN - 1) / TBN;
   const int64_t tiles = tiles_m * tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  kern<<<(unsigned)tiles, TNT, TT_SMEM, p.stream>>>(static_cast<float*>(p.c), p.M, p.N, p.K, p.ldc,
-                                                    special, tiles_m, tiles_n, map_a, map_b);
+  kern<<<(unsigned)tiles, TT::THREADS, TT::SMEM, p.stream>>>(
+      static_cast<float*>(p.c), p.M, p.N, p.K, p.ldc, special, tiles_m, tiles_n, map_a, map_b);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int C, int R, int MODE, bool ACC>
 cudaError_t tropical_launch(const Problem& p, const unsigned* special) {
-  // TMA-staged kernel when the layout allows it: 19.5 vs 18.6 T pairs/s at c5
-  // (profiles/r01_tune_tropical_tma.jsonl); bit-identical results
-  // Four k per step (B rows in registers, 16-byte A loads) once the grid fills
-  // both CTA slots of every SM: 222.2 vs 228.7 ms at c5; on grids below that
-  // the shorter two-k step wins (profiles/r01_tune_tropical_quad.jsonl)
-  if (tropical_tma_eligible(p)) {
-    const int64_t tiles = ((p.M + TBM - 1) / TBM) * ((p.N + TBN - 1) / TBN);
-    return tiles >= 2 * kNumSMs ? tropical_tma_launch<C, R, MODE, ACC, 2, 1, true>(p, special)
-                                : tropical_tma_launch<C, R, MODE, ACC>(p, special);
-  }
+  // TMA-staged kernel when the layout allows it (the first TMA version: 19.5
+  // vs 18.6 T pairs/s at c5, profiles/r01_tune_tropical_tma.jsonl); bit-identical
+  // 64 x 128 CTA tiles of 128 threads, three per SM (up to 168 registers per
+  // thread), stepping four k at a time (B rows in registers, 16-byte A loads):
+  // c5 217.9 ms vs 222.4 ms for 128 x 128 tiles of 256 threads (two per SM,
+  // 128 registers) and 228.7 ms for those with the two-k step; 1000^3
+  // 0.089 vs 0.146 ms (twice the CTAs) — profiles/r01_tune_tropical_quad.jsonl,
+  // r01_tune_tropical_bm64.jsonl
+  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE, ACC, 3, 1, true, 64>(p, special);
   const bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);

@@ -53,7 +53,7 @@ void trial_tropical(const moa::Problem& p0, float* out, float* ref, unsigned* sp
   fflush(stdout);
 }
 
-template <int MINB, int UNR, bool QUAD = false>
+template <int MINB, int UNR, bool QUAD = false, int BMT = 128>
 void trial_tma(const moa::Problem& p0, float* out, float* ref, unsigned* special,
                unsigned long long* cnt) {
   moa::Problem p = p0;
@@ -62,12 +62,12 @@ void trial_tma(const moa::Problem& p0, float* out, float* ref, unsigned* special
   cudaEvent_t s, e;
   CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
   CK(cudaMemset(out, 0, (size_t)p.M * p.N * 4));
-  CK((moa::tropical_tma_launch<0, 2, 2, false, MINB, UNR, QUAD>(p, special)));
+  CK((moa::tropical_tma_launch<0, 2, 2, false, MINB, UNR, QUAD, BMT>(p, special)));
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < 2; r++) {
     CK(cudaEventRecord(s));
-    CK((moa::tropical_tma_launch<0, 2, 2, false, MINB, UNR, QUAD>(p, special)));
+    CK((moa::tropical_tma_launch<0, 2, 2, false, MINB, UNR, QUAD, BMT>(p, special)));
     CK(cudaEventRecord(e)); CK(cudaEventSynchronize(e));
     float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
   }
@@ -76,8 +76,8 @@ void trial_tma(const moa::Problem& p0, float* out, float* ref, unsigned* special
   count_diff<<<1184, 256>>>(out, ref, (size_t)p.M * p.N, cnt);
   CK(cudaMemcpy(&diff, cnt, 8, cudaMemcpyDeviceToHost));
   const double pairs = (double)p.M * p.N * p.K;
-  printf("{\"kernel\": \"tropical_tma_minb%d_unr%d%s\", \"M\": %ld, \"K\": %ld, \"N\": %ld, \"ms\": %.3f, \"Gpairs_s\": %.1f, \"frac_of_24475\": %.4f, \"bit_diffs\": %llu}\n",
-         MINB, UNR, QUAD ? "_quad" : "", (long)p.M, (long)p.K, (long)p.N, best, pairs / (best * 1e-3) / 1e9, pairs / (best * 1e-3) / 1e9 / 24475.4, diff);
+  printf("{\"kernel\": \"tropical_tma_bm%d_minb%d_unr%d%s\", \"M\": %ld, \"K\": %ld, \"N\": %ld, \"ms\": %.3f, \"Gpairs_s\": %.1f, \"frac_of_24475\": %.4f, \"bit_diffs\": %llu}\n",
+         BMT, MINB, UNR, QUAD ? "_quad" : "", (long)p.M, (long)p.K, (long)p.N, best, pairs / (best * 1e-3) / 1e9, pairs / (best * 1e-3) / 1e9 / 24475.4, diff);
   fflush(stdout);
 }
 
@@ -121,21 +121,24 @@ int main() {
   CK(cudaMemcpy(special, flags, 8, cudaMemcpyHostToDevice));
   moa::Problem p{MOA_DTYPE_F32, ref, a, b, n, n, n, n, n, n, 0, 2, false, 0};
   trial<8, 8, 2>(p, ref, ref, special, cnt);  // exact loop: the reference bits
-  trial_tma<2, 1>(p, c, ref, special, cnt);
   trial_tma<2, 1, true>(p, c, ref, special, cnt);
-  trial_tma<1, 1, true>(p, c, ref, special, cnt);
-  trial_tma<2, 1>(p, c, ref, special, cnt);
+  trial_tma<3, 1, true, 64>(p, c, ref, special, cnt);
+  trial_tma<3, 2, true, 64>(p, c, ref, special, cnt);
+  trial_tma<3, 1, false, 64>(p, c, ref, special, cnt);
   trial_tma<2, 1, true>(p, c, ref, special, cnt);
   // ragged shape: K odd (lone-k tail), M/N not tile multiples
   moa::Problem q{MOA_DTYPE_F32, ref, a, b, 1000, 1001, 1004, 1004, 1004, 1004, 0, 2, false, 0};
   CK((moa::semiring_launch<float, 0, 2, false, -1>(q, special)));
   trial_tma<2, 1>(q, c, ref, special, cnt);
   trial_tma<2, 1, true>(q, c, ref, special, cnt);
+  trial_tma<3, 1, true, 64>(q, c, ref, special, cnt);
   moa::Problem q2{MOA_DTYPE_F32, ref, a, b, 1000, 1002, 1004, 1004, 1004, 1004, 0, 2, false, 0};
   CK((moa::semiring_launch<float, 0, 2, false, -1>(q2, special)));
   trial_tma<2, 1, true>(q2, c, ref, special, cnt);
+  trial_tma<3, 1, true, 64>(q2, c, ref, special, cnt);
   moa::Problem q3{MOA_DTYPE_F32, ref, a, b, 1000, 1003, 1004, 1004, 1004, 1004, 0, 2, false, 0};
   CK((moa::semiring_launch<float, 0, 2, false, -1>(q3, special)));
   trial_tma<2, 1, true>(q3, c, ref, special, cnt);
+  trial_tma<3, 1, true, 64>(q3, c, ref, special, cnt);
   return 0;
 }
