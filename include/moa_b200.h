@@ -128,6 +128,11 @@ const char* moa_last_error(void);
 /* ABI version (major*100 + minor). */
 int moa_abi_version(void);
 
+/* Number of CUDA devices visible to this process (0 if none or on error):
+   lets a host binding spread the reference's execute_parallel workers over
+   the GPUs (worker k -> device k mod count). */
+int moa_device_count(void);
+
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t moa_launch_count(void);
 

@@ -13,9 +13,13 @@ caller's rows of res, so concurrent callers never overwrite each other's
 rows.  Nothing but ctypes and numpy is imported; no torch in the reference's
 process.
 
-The library is found through $MOA_B200_LIB (default: the in-tree build), the
-GPU through $MOA_B200_DEVICE (default 0).  Registration in the reference's
-_backend.py (:5-14) is two lines; see INTEGRATION.md.
+The reference's execute_parallel calls this from W threads, worker k with
+rows k, k+W, ... (parallel.py:37-43); worker k runs on GPU DEVICES[k mod
+len(DEVICES)], so the reference's own fork-join spreads its row sets over the
+GPUs of the box.  The library is found through $MOA_B200_LIB (default: the
+in-tree build), the GPUs through $MOA_B200_DEVICES (comma-separated indices;
+default: every visible device).  Registration in the reference's _backend.py
+(:5-14) is two lines; see INTEGRATION.md.
 """
 
 from __future__ import annotations
@@ -37,9 +41,12 @@ _lib.moa_product_rows_host.argtypes = _ARGS + [ctypes.c_int]        # ... flags,
 _lib.moa_product_rows.restype = ctypes.c_int
 _lib.moa_product_rows.argtypes = _ARGS + [ctypes.c_void_p]          # ... flags, stream
 _lib.moa_last_error.restype = ctypes.c_char_p
+_lib.moa_device_count.restype = ctypes.c_int
 MOA_DTYPE_F64 = 0
 MOA_FLAG_ACCUMULATE = 1
-DEVICE = int(os.environ.get("MOA_B200_DEVICE", "0"))
+DEVICES = ([int(d) for d in os.environ["MOA_B200_DEVICES"].split(",") if d.strip()]
+           if os.environ.get("MOA_B200_DEVICES") else
+           list(range(max(1, _lib.moa_device_count()))))
 
 
 def product_rows(res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restride,
@@ -53,6 +60,6 @@ def product_rows(res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restri
     rc = _lib.moa_product_rows_host(MOA_DTYPE_F64, res.ctypes.data, a.ctypes.data, b.ctypes.data,
                                     noproc, rowsinred, elsinop, lstride, rstride, restride,
                                     combine_code, reduce_code, start, step,
-                                    MOA_FLAG_ACCUMULATE, DEVICE)
+                                    MOA_FLAG_ACCUMULATE, DEVICES[start % len(DEVICES)])
     if rc != 0:
         raise RuntimeError(_lib.moa_last_error().decode())

@@ -24,7 +24,7 @@ FLAG_EXACT = 2
 
 # every symbol include/moa_b200.h declares
 EXPORTS = ("moa_product_rows", "moa_product_rows_host", "moa_last_error", "moa_abi_version",
-           "moa_launch_count", "moa_plan_kernel")
+           "moa_device_count", "moa_launch_count", "moa_plan_kernel")
 
 _lock = threading.Lock()
 _lib: ctypes.CDLL | None = None
@@ -48,6 +48,8 @@ def _bind(lib: ctypes.CDLL) -> None:
     lib.moa_last_error.argtypes = []
     lib.moa_abi_version.restype = ctypes.c_int
     lib.moa_abi_version.argtypes = []
+    lib.moa_device_count.restype = ctypes.c_int
+    lib.moa_device_count.argtypes = []
     lib.moa_launch_count.restype = ctypes.c_uint64
     lib.moa_launch_count.argtypes = []
     lib.moa_plan_kernel.restype = ctypes.c_char_p

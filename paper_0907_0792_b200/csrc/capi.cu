@@ -61,7 +61,16 @@ const char* route_name(Route r) {
 
 extern "C" {
 
-int moa_abi_version(void) { return 100; }
+int moa_abi_version(void) { return 101; }
+
+int moa_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
 
 const char* moa_last_error(void) { return t_last_error.c_str(); }
 

@@ -31,7 +31,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert set(decl) == set(_native.EXPORTS)
     for name in decl:
         assert hasattr(lib, name), name
-    assert _native.abi_version() == 100
+    assert _native.abi_version() == 101  # 1.01: moa_product_rows_host, moa_device_count
 
 
 def test_header_constants_match_python_codes():

@@ -76,3 +76,24 @@ def test_reference_style_outer_and_empty_rows(rng):
     before = res.copy()
     mod.product_rows(res, x, y, 40, 1, 70, 1, 70, 70, 2, 0, 45, 3)  # surplus worker: no rows
     assert_bits_equal(res, before)
+
+
+@pytest.mark.gpu
+def test_workers_spread_over_listed_devices(monkeypatch, rng):
+    """$MOA_B200_DEVICES lists the GPUs; worker k of the reference's
+    execute_parallel (rows k::W) runs on DEVICES[k mod len].  On a one-GPU box
+    the list repeats device 0, which exercises the mapping."""
+    monkeypatch.setenv("MOA_B200_DEVICES", "0,0,0")
+    mod = _module()
+    assert mod.DEVICES == [0, 0, 0]
+    m, k, n = 97, 40, 61
+    a, b = rng.random(m * k), rng.random(k * n)
+    ops = moa.op_pair("subtract", "min")
+    c, r = ops.codes()
+    res = np.full(m * n, ops.reduce_identity)
+    workers = 5
+    with ThreadPoolExecutor(workers) as pool:
+        for f in [pool.submit(mod.product_rows, res, a, b, m, k, n, k, n, n, c, r, w, workers)
+                  for w in range(workers)]:
+            f.result()
+    assert_bits_equal(res, oracle.product(a, b, m, k, n, c, r))
