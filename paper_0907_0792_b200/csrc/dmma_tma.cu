@@ -99,6 +99,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   const int wm0 = (warp / (Cfg::BN / Cfg::WN)) * Cfg::WM, wn0 = (warp % (Cfg::BN / Cfg::WN)) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
 
+  // The first TMA loads are issued only after the block barrier that follows
+  // the mbarrier init: issuing them between the init fence and __syncthreads
+  // (to overlap the first round trip with setup) corrupted a few warps' results
+  // in accumulate-mode launches, intermittently (caught by
+  // tests/test_gpu_host_abi.py; tests/test_gpu_parity.py::
+  // test_dmma_accumulate_launches_repeat_bitwise guards it).
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < Cfg::STAGES; s++) {

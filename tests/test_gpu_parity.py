@@ -430,6 +430,33 @@ def test_dmma_tiny_tma_bitwise_equal_cp_async_path(mkn, rng):
     torch.cuda.synchronize()
 
 
+def test_dmma_accumulate_launches_repeat_bitwise(rng):
+    """Accumulate-mode TMA DMMA launches over a zero-filled C, repeated: every
+    one equals the write-only launch bit for bit (an mbarrier-init / TMA-issue
+    ordering race once broke a few warps' results intermittently, only in
+    this mode); the float32 tropical TMA kernel likewise."""
+    torch = _torch()
+    m, k, n = 2048, 96, 16384
+    a, b = _dev(rng.random(m * k) * 100), _dev(rng.random(k * n) * 100)
+    plan = plan_inner((m, k), (k, n))
+    want = torch.empty(m * n, dtype=torch.float64, device="cuda")
+    launch(plan, want, a, b, moa.MUL_ADD)
+    c = torch.empty_like(want)
+    for trial in range(12):
+        c.zero_()
+        launch(plan, c, a, b, moa.MUL_ADD, accumulate=True)
+        assert torch.equal(c, want), f"accumulate launch {trial}"
+    ops = op_pair("add", "min")
+    a32, b32 = a.float(), b.float()
+    want32 = torch.empty(m * n, dtype=torch.float32, device="cuda")
+    launch(plan, want32, a32, b32, ops)
+    c32 = torch.empty_like(want32)
+    for trial in range(6):
+        c32.fill_(float("inf"))
+        launch(plan, c32, a32, b32, ops, accumulate=True)
+        assert torch.equal(c32, want32), f"tropical accumulate launch {trial}"
+
+
 @pytest.mark.parametrize("dt,mkn", [(np.float32, (257, 131, 300)),   # odd K, unaligned: cp.async
                                     (np.float32, (1000, 132, 1004)),  # 16-byte rows: TMA kernel
                                     (np.float64, (257, 131, 300))])   # exact fold, specials
