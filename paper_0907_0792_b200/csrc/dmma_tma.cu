@@ -99,12 +99,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   const int wm0 = (warp / (Cfg::BN / Cfg::WN)) * Cfg::WM, wn0 = (warp % (Cfg::BN / Cfg::WN)) * Cfg::WN;
   const int g = lane >> 2, t = lane & 3;
 
-  // The first TMA loads are issued only after the block barrier that follows
-  // the mbarrier init: issuing them between the init fence and __syncthreads
-  // (to overlap the first round trip with setup) corrupted a few warps' results
-  // in accumulate-mode launches, intermittently (caught by
-  // tests/test_gpu_host_abi.py; tests/test_gpu_parity.py::
-  // test_dmma_accumulate_launches_repeat_bitwise guards it).
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < Cfg::STAGES; s++) {
@@ -183,8 +177,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 #pragma unroll
         for (int ni = 0; ni < Cfg::NI; ni++) dmma_step(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    tma::release_stage(&empty[stage], lane);
     // refill the slab of iteration kt-1 with k-slab kt-1+STAGES
     if (tid == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
       const int ps = (int)((kt - 1) % Cfg::STAGES);
@@ -317,8 +310,7 @@ __global__ void __launch_bounds__(TinyCfg::THREADS, 1)
 #pragma unroll
     for (int kk = 0; kk < T::BK; kk += 4)
       dmma_step(acc, a0p[kk], a1p[kk], bp[kk * T::B_PITCH]);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    tma::release_stage(&empty[stage], lane);
     if (tid == 0 && kt >= 1 && kt - 1 + STAGES < KT) {
       const int ps = (int)((kt - 1) % STAGES);
       mbar_wait(&empty[ps], (unsigned)(((kt - 1) / STAGES) & 1));

@@ -268,9 +268,13 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     const Block& bl = blocks[i];
     const int slot = (int)(i % nslots);
     const int64_t nr = bl.r1 - bl.r0;
-    // --- in: this block's A rows (and res rows when accumulating), B behind block 0
+    // --- in: this block's A rows (and res rows when accumulating), B behind block 0.
+    // The first block, computed per k-chunk, takes its A rows in the same
+    // k-chunks (2-D copies of a column range), each just ahead of the matching
+    // B chunk, so the first kernel waits for one chunk of each, not all of A0.
+    const bool a_by_chunk = i == 0 && chunks.size() > 1 && a_dense;
     if (a_free[slot]) ss.check(cudaStreamWaitEvent(ss.s_in, a_free[slot], 0));
-    if (K > 0) {
+    if (K > 0 && !a_by_chunk) {
       if (a_dense)
         ss.check(cudaMemcpy2DAsync(a_buf[slot], (size_t)K * esz,
                                    a_rows + (size_t)(bl.r0 * lstride * step) * esz,
@@ -291,6 +295,12 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     ss.check(cudaEventRecord(a_ready, ss.s_in));
     if (i == 0 && K > 0) {
       for (const auto& ch : chunks) {
+        if (a_by_chunk)
+          ss.check(cudaMemcpy2DAsync(a_buf[slot] + (size_t)ch.first * esz, (size_t)K * esz,
+                                     a_rows + (size_t)(bl.r0 * lstride * step + ch.first) * esz,
+                                     (size_t)(lstride * step) * esz,
+                                     (size_t)(ch.second - ch.first) * esz, (size_t)nr,
+                                     cudaMemcpyHostToDevice, ss.s_in));
         if (b_dense)
           ss.check(cudaMemcpy2DAsync(b_buf + (size_t)(ch.first * N) * esz, (size_t)N * esz,
                                      static_cast<const char*>(b) + (size_t)(ch.first * rstride) * esz,

@@ -35,6 +35,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
+// A consumer's release of a stage that TMA (the async proxy) will overwrite:
+// every lane orders its shared-memory reads of the stage before the async
+// proxy's next writes (fence.proxy.async), the warp converges, and one lane
+// arrives on the stage's `empty` barrier.  Without the fence ptxas may hoist the
+// arrive above the slab's last fragment loads, so the producer's refill can
+// land before they read — seen as intermittent corruption of a few warps'
+// results (tests/test_gpu_parity.py::test_dmma_accumulate_launches_repeat_bitwise).
+__device__ __forceinline__ void release_stage(uint64_t* empty_bar, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty_bar);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"

@@ -403,8 +403,7 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
                 ReduceOp<R>::f(acc[i][4 * g + cc], CombineOp<C>::f(av, bs[k * TBN + 64 * g + cc]));
       }
     }
-    __syncwarp();
-    if (lane == 0) tma::mbar_arrive(&empty[stage]);
+    tma::release_stage(&empty[stage], lane);
     // refill the slab consumed one iteration ago (its readers are long done)
     if (tid == 0 && kt >= 1 && kt - 1 + TSTAGES < KT) {
       const int ps = (int)((kt - 1) % TSTAGES);

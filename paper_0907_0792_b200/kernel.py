@@ -323,168 +323,34 @@ def execute_sequential(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair =
                        *, backend: str | None = None, exact: bool = False) -> MoaArray:
     """Run the planned product over all result rows.
 
-    Device operands: one launch.  Host operands of a large product: the rows
-    are streamed in blocks (``_stream_chunks``) so the copy of A's next block
-    and of C's previous block overlap the kernel; the bits are those of one
-    launch because rows are independent.
+    Device operands: one launch.  Host operands: the native executor
+    (``execute_host``), which streams large products in row blocks so the
+    copies overlap the kernels; the bits are those of one launch because rows
+    are independent.
     """
     if not (a.is_device or b.is_device):
-        blocks = _stream_blocks(plan, result_dtype(a, b), ops)
-        if len(blocks) > 1:
-            _check_plan(plan, a, b)
-            resolve_backend(backend, ops)
-            return _execute_streamed(plan, a, b, ops, blocks, exact=exact)
+        _check_plan(plan, a, b)
+        resolve_backend(backend, ops)
+        return execute_host(plan, a, b, ops, exact=exact)
     runner = _Runner(plan, a, b, ops, backend, exact=exact)
     runner.run_rows(0, 1)
     return runner.finish()
 
 
-_STREAM_MIN_OUT_BYTES = 128 << 20
-_WAVES_PER_CHUNK = 24  # >= 24 waves of CTAs per block keeps the tail wave small
-
-
-_EDGE_MIN_WAVES = 6    # ... and >= 6 waves in each half-size end block
-
-
-def edge_blocks(noproc: int, middle: int = 3, align: int = 128) -> list[range]:
-    """Row blocks for streaming: a 3/16 first block, ``middle`` equal blocks,
-    a 1/16 last block (sizes rounded to ``align`` rows).  The first block is
-    computed k-chunk by k-chunk while B lands, so it must be long enough to
-    cover B's transfer and the next block's A rows (B is 16% of c4's compute
-    time at the measured host link); the last block's C rows are the copy no
-    compute can hide, so it is small.  Middle blocks stay long enough that
-    their partial last wave of CTAs costs little.  (A copy/compute timeline
-    model over the BASELINE configs picked these fractions: c4 273 -> 260 ms
-    against half-size end blocks.)"""
-    from .parallel import row_blocks  # local: parallel imports this module
-    first = noproc * 3 // 16
-    first -= first % align
-    last = noproc // 16
-    last -= last % align
-    if first <= 0 or last <= 0:
-        return row_blocks(noproc, middle + 2)
-    mid = noproc - first - last
-    size = -(-mid // middle)
-    size += -size % align
-    bounds = [0] + [min(first + i * size, noproc - last) for i in range(middle)] + \
-        [noproc - last, noproc]
-    return [range(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1)
-            if bounds[i + 1] > bounds[i]]
-
-
-def _stream_blocks(plan: KernelPlan, dtype: np.dtype, ops: OpPair = MUL_ADD) -> list[range]:
-    """Row blocks for the streamed host path (one block = do not stream)."""
-    from .parallel import row_blocks  # local: parallel imports this module
-    m = plan.noproc
-    if plan.rowsinred < 2:  # outer products are pure D2H; blocks cannot hide it
-        return [range(0, m)]
-    out_bytes = m * plan.elsinop * np.dtype(dtype).itemsize
-    if ops.codes() == (2, 0) and np.dtype(dtype) == np.dtype(np.float64):
-        tiles, per_wave = -(-m // 64) * -(-plan.elsinop // 128), 296  # dmma.cu
-    else:
-        tiles, per_wave = -(-m // 128) * -(-plan.elsinop // 128), 296  # semiring.cu
-    if out_bytes >= 8 * _STREAM_MIN_OUT_BYTES and tiles >= 8 * _EDGE_MIN_WAVES * per_wave:
-        return edge_blocks(m)
-    by_waves = tiles // (per_wave * _WAVES_PER_CHUNK)
-    return row_blocks(m, int(max(1, min(8, out_bytes // _STREAM_MIN_OUT_BYTES, by_waves))))
-
-
-def _execute_streamed(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair, chunks,
-                      *, exact: bool = False, device=None) -> MoaArray:
-    """Host operands -> host result with copies overlapped with compute.
-
-    For each row block: H2D of its A rows on a copy stream, the kernel on the
-    compute stream, D2H of its C rows on a second copy stream, with two-deep
-    device buffers.  Every row needs all of B, so a host B is copied in
-    slab-aligned k-chunks behind the first block's A rows, and the first
-    block is computed chunk by chunk as they land (later chunks accumulate,
-    MOA_FLAG_ACCUMULATE; the same k order, so the same bits, whenever the fold
-    is stored in its own type) — B's transfer then hides behind compute
-    instead of preceding it.
-    """
-    from .distributed import k_chunks  # local: distributed imports this module
-    from .parallel import row_blocks  # local: parallel imports this module
+def execute_host(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair = MUL_ADD, *,
+                 exact: bool = False, device=None) -> MoaArray:
+    """Host operands -> host result through the native executor
+    (moa_product_rows_host, csrc/host_exec.cu): A, B and the result move with
+    2-D copies, large products stream in row blocks with the copies
+    overlapping the kernels (B in k-chunks behind the first block), and the
+    result lands in page-locked memory so its copy-back runs at link speed."""
     torch = _torch()
     _native.load()
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else \
-        torch.device(device)
     dtype = result_dtype(a, b)
-    tdt = torch_dtype(dtype)
-    m, n, lda = plan.noproc, plan.elsinop, plan.lstride
-    comp = torch.cuda.current_stream(dev)
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    out = torch.empty(m * n, dtype=tdt, pin_memory=True)
-    # chunks: a number of equal row blocks, or the blocks themselves
-    blocks = [r for r in (row_blocks(m, chunks) if isinstance(chunks, int) else chunks) if len(r)]
-    k = plan.rowsinred
-    # k-chunks accumulate through the result buffer, so the fold must not be
-    # carried in a wider type than it is stored in (float32 data folded in
-    # float64: sums, products, and multiply/divide with min/max)
-    wide = np.dtype(dtype) == np.float32 and (ops.reduce_name in ("add", "multiply") or
-                                              ops.combine_name in ("multiply", "divide"))
-    chunked = not b.is_device and not wide
-    # the first block takes B in k-chunks as they land; with half-size end
-    # blocks, eight chunks keep that block's per-chunk compute above the
-    # per-chunk transfer while the first chunk (the exposed part) stays small
-    b_chunks = k_chunks(k, 8 if len(blocks) >= 5 else len(blocks)) if chunked else [(0, k)]
-    if not chunked:
-        b_dev = stage(b, dev, dtype)
-        b_ready = [None]
-    else:
-        b_dev = torch.empty(k * n, dtype=tdt, device=dev)
-        host_b = b.data if b.data.dtype == dtype else b.data.astype(dtype)
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore", UserWarning)
-            host_b_t = torch.from_numpy(host_b)
-        b_ready = []
-    rows_max = max(len(r) for r in blocks)
-    a_buf = [torch.empty(rows_max * lda, dtype=tdt, device=dev) for _ in range(2)]
-    c_buf = [torch.empty(rows_max * n, dtype=tdt, device=dev) for _ in range(2)]
-    a_free = [None, None]
-    c_free = [None, None]
-    host_a = a.data if a.data.dtype == dtype else a.data.astype(dtype)
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore", UserWarning)
-        host_a_t = torch.from_numpy(host_a)
-    for idx, rows in enumerate(blocks):
-        slot, r0, r1 = idx % 2, rows.start, rows.stop
-        na, nc = (r1 - r0) * lda, (r1 - r0) * n
-        with torch.cuda.stream(s_in):
-            if a_free[slot] is not None:
-                s_in.wait_event(a_free[slot])
-            a_buf[slot][:na].copy_(host_a_t[r0 * lda:r1 * lda], non_blocking=True)
-            a_ready = torch.cuda.Event()
-            a_ready.record(s_in)
-            if idx == 0 and chunked:  # B's k-chunks queue behind block 0's rows
-                for k0, k1 in b_chunks:
-                    b_dev[k0 * n:k1 * n].copy_(host_b_t[k0 * n:k1 * n], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(s_in)
-                    b_ready.append(ev)
-        comp.wait_event(a_ready)
-        if c_free[slot] is not None:
-            comp.wait_event(c_free[slot])
-        if idx == 0:
-            for j, (k0, k1) in enumerate(b_chunks):
-                if b_ready[j] is not None:
-                    comp.wait_event(b_ready[j])
-                part = KernelPlan(plan.mode, r1 - r0, k1 - k0, n, lda, plan.rstride, plan.restride,
-                                  plan.result_shape)
-                launch(part, c_buf[slot][:nc], a_buf[slot][k0:na], b_dev[k0 * n:], ops,
-                       exact=exact, accumulate=j > 0, stream=comp)
-        else:
-            sub = KernelPlan(plan.mode, r1 - r0, k, n, lda, plan.rstride, plan.restride,
-                             plan.result_shape)
-            launch(sub, c_buf[slot][:nc], a_buf[slot][:na], b_dev, ops, exact=exact, stream=comp)
-        done = torch.cuda.Event()
-        done.record(comp)
-        a_free[slot] = done
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(done)
-            out[r0 * n:r1 * n].copy_(c_buf[slot][:nc], non_blocking=True)
-            copied = torch.cuda.Event()
-            copied.record(s_out)
-            c_free[slot] = copied
-    s_out.synchronize()
-    comp.synchronize()
-    return MoaArray._wrap(plan.result_shape, out.numpy())
+    host_a = np.ascontiguousarray(a.data if a.data.dtype == dtype else a.data.astype(dtype)).ravel()
+    host_b = np.ascontiguousarray(b.data if b.data.dtype == dtype else b.data.astype(dtype)).ravel()
+    n_out = plan.noproc * plan.elsinop
+    out = torch.empty(n_out, dtype=torch_dtype(dtype), pin_memory=True).numpy()
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    launch_host(plan, out, host_a, host_b, ops, exact=exact, device=dev)
+    return MoaArray._wrap(plan.result_shape, out)

@@ -21,7 +21,7 @@ from __future__ import annotations
 
 from . import _native
 from .arrays import MoaArray
-from .kernel import (KernelPlan, _Runner, _check_plan, launch, resolve_backend,
+from .kernel import (KernelPlan, _Runner, _check_plan, execute_host, launch, resolve_backend,
                      result_dtype, stage, stage_host, torch_dtype)
 from .ops import MUL_ADD, OpPair
 
@@ -62,6 +62,11 @@ def execute_parallel(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair = M
         devices = list(range(torch.cuda.device_count())) or [0]
     devices = list(devices)[:workers]
     if len(devices) <= 1:
+        if not (a.is_device or b.is_device):  # host operands: the native executor
+            _check_plan(plan, a, b)
+            resolve_backend(backend, ops)
+            return execute_host(plan, a, b, ops, exact=exact,
+                                device=devices[0] if devices else None)
         runner = _Runner(plan, a, b, ops, backend, exact=exact,
                          device=None if not devices else _device_for(a, b, devices[0]))
         runner.run_rows(0, 1)

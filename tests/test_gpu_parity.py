@@ -767,24 +767,31 @@ def test_launch_counter_advances():
     assert _native.launch_count() > before
 
 
-def test_streamed_host_path_bitwise_equals_one_launch(rng):
-    """Host operands of large products go through row blocks with overlapped
-    copies (kernel._execute_streamed); the bits equal one device launch."""
-    from paper_0907_0792_b200.kernel import _execute_streamed, edge_blocks
+def test_host_operands_through_native_executor_equal_device_launch(rng):
+    """Host operands go through the native executor (moa_product_rows_host):
+    the public API's result equals one device launch bit for bit, for float64
+    and float32 pairs (fast folds, float64-folded float32, exact division),
+    mixed-dtype operands, and through execute_parallel on one GPU.  (The
+    streamed row-block schedule is covered at >= 1 GiB in
+    tests/test_gpu_host_abi.py.)"""
     m, k, n = 1000, 300, 777
     a = rng.random(m * k) * 2 - 1
     b = rng.random(k * n) * 2 - 1
-    # float64 / fast-fold float32 pairs stream B in k-chunks (accumulating);
-    # float32 pairs folded in float64 take B in one piece
     for ops, dt in ((op_pair("multiply", "add"), np.float64), (op_pair("add", "min"), np.float32),
                     (op_pair("max", "multiply"), np.float64), (op_pair("divide", "max"), np.float64),
                     (op_pair("multiply", "add"), np.float32), (op_pair("subtract", "max"), np.float32)):
         A, B = MoaArray((m, k), a, dtype=dt), MoaArray((k, n), b, dtype=dt)
         want = moa.inner(A.to_device(), B.to_device(), ops).host_data()
-        for chunks in (2, 3, 7, edge_blocks(m, 3, 16)):
-            got = _execute_streamed(moa.plan_inner(A.shape, B.shape), A, B, ops, chunks)
-            assert got.shape == (m, n)
-            assert_bits_equal(got.data, want, f"{ops} chunks={chunks}")
+        got = moa.inner(A, B, ops)
+        assert got.shape == (m, n) and got.data.dtype == np.dtype(dt)
+        assert_bits_equal(got.data, want, f"{ops} {dt.__name__}")
+        assert_bits_equal(moa.execute_parallel(moa.plan_inner(A.shape, B.shape), A, B, ops,
+                                               workers=1).data, want, f"{ops} parallel")
+    # mixed float32 x float64 operands compute in float64
+    A32 = MoaArray((m, k), a, dtype=np.float32)
+    B64 = MoaArray((k, n), b)
+    want = moa.inner(A32.to_device(), B64.to_device(), op_pair("add", "min")).host_data()
+    assert_bits_equal(moa.inner(A32, B64, op_pair("add", "min")).data, want, "mixed dtypes")
 
 
 def test_kernels_never_write_outside_their_rows(rng):
