@@ -436,13 +436,13 @@ def test_dmma_accumulate_launches_repeat_bitwise(rng):
     ordering race once broke a few warps' results intermittently, only in
     this mode); the float32 tropical TMA kernel likewise."""
     torch = _torch()
-    m, k, n = 2048, 96, 16384
+    m, k, n = 4096, 256, 4096  # ~1 launch in 20 went wrong here before the fix
     a, b = _dev(rng.random(m * k) * 100), _dev(rng.random(k * n) * 100)
     plan = plan_inner((m, k), (k, n))
     want = torch.empty(m * n, dtype=torch.float64, device="cuda")
     launch(plan, want, a, b, moa.MUL_ADD)
     c = torch.empty_like(want)
-    for trial in range(12):
+    for trial in range(80):
         c.zero_()
         launch(plan, c, a, b, moa.MUL_ADD, accumulate=True)
         assert torch.equal(c, want), f"accumulate launch {trial}"
@@ -451,7 +451,7 @@ def test_dmma_accumulate_launches_repeat_bitwise(rng):
     want32 = torch.empty(m * n, dtype=torch.float32, device="cuda")
     launch(plan, want32, a32, b32, ops)
     c32 = torch.empty_like(want32)
-    for trial in range(6):
+    for trial in range(30):
         c32.fill_(float("inf"))
         launch(plan, c32, a32, b32, ops, accumulate=True)
         assert torch.equal(c32, want32), f"tropical accumulate launch {trial}"
