@@ -446,6 +446,17 @@ def test_dmma_accumulate_launches_repeat_bitwise(rng):
         c.zero_()
         launch(plan, c, a, b, moa.MUL_ADD, accumulate=True)
         assert torch.equal(c, want), f"accumulate launch {trial}"
+    # the 16x32-tile TMA kernel with its ring refilling (K = 1024 > 8 stages x 32)
+    mt, kt_, nt = 256, 1024, 256
+    at, bt = _dev(rng.random(mt * kt_) * 100), _dev(rng.random(kt_ * nt) * 100)
+    plan_t = plan_inner((mt, kt_), (kt_, nt))
+    want_t = torch.empty(mt * nt, dtype=torch.float64, device="cuda")
+    launch(plan_t, want_t, at, bt, moa.MUL_ADD)
+    ct = torch.empty_like(want_t)
+    for trial in range(80):
+        ct.zero_()
+        launch(plan_t, ct, at, bt, moa.MUL_ADD, accumulate=True)
+        assert torch.equal(ct, want_t), f"16x32-tile accumulate launch {trial}"
     ops = op_pair("add", "min")
     a32, b32 = a.float(), b.float()
     want32 = torch.empty(m * n, dtype=torch.float32, device="cuda")
