@@ -9,8 +9,8 @@
 // reference's execute_parallel, parallel.py:26-43) never touch each other's
 // rows.
 //
-// Large products are streamed (the same schedule as the Python host path,
-// kernel._execute_streamed): row blocks with a 3/16 first block, three middle
+// Large products are streamed (the public Python API's host path runs through
+// here too, kernel.execute_host): row blocks with a 3/16 first block, three middle
 // blocks and a 1/16 last block; A rows of the next block copy in on one
 // stream while the current block computes on another and the previous block's
 // rows copy out on a third, double-buffered.  Every row needs all of B, so B
