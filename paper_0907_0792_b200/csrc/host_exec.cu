@@ -20,6 +20,7 @@
 // float32 data folded in float64).  Copies overlap the kernels when the host
 // buffers are page-locked; pageable buffers are staged by the driver (same
 // results, lower bandwidth).
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -41,15 +42,48 @@ struct Block {
   int64_t r0, r1;  // rows of the row set (0-based, in units of the set)
 };
 
-std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K) {
-  if (K < 2 || out_bytes < 8 * kStreamMinOutBytes) return {{0, rows}};
+// A rows + C rows of one block: 4 GiB ($MOA_HOST_BLOCK_BYTES overrides it, so
+// tests can exercise the multi-block schedules at small sizes)
+int64_t max_block_bytes() {
+  if (const char* e = std::getenv("MOA_HOST_BLOCK_BYTES")) {
+    const long long v = std::atoll(e);
+    if (v > 0) return v;
+  }
+  return 4ll << 30;
+}
+
+// Row blocks of the set: one block below 1 GiB of result; outer products (and
+// K = 0) in equal blocks of at most max_block_bytes(), whose copy-out overlaps
+// the next block's kernel; inner products as a 3/16 first block (computed per
+// k-chunk of B), middle blocks, a 1/16 last block, every block within
+// max_block_bytes() so device memory stays bounded (two slots of each buffer).
+std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K, int64_t row_bytes) {
+  const int64_t cap_bytes = max_block_bytes();
+  if (out_bytes < 8 * kStreamMinOutBytes && out_bytes <= cap_bytes) return {{0, rows}};
+  const int64_t cap_rows = cap_bytes / (row_bytes > 0 ? row_bytes : 1);
+  if (K < 2) {
+    if (rows <= cap_rows || cap_rows < 1) return {{0, rows}};
+    const int64_t nb = (rows + cap_rows - 1) / cap_rows, size = (rows + nb - 1) / nb;
+    std::vector<Block> out;
+    for (int64_t r = 0; r < rows; r += size) out.push_back({r, r + size < rows ? r + size : rows});
+    return out;
+  }
   int64_t first = rows * 3 / 16, last = rows / 16;
+  if (cap_rows >= kRowAlign) {
+    first = first < cap_rows ? first : cap_rows;
+    last = last < cap_rows ? last : cap_rows;
+  }
   first -= first % kRowAlign;
   last -= last % kRowAlign;
   if (first <= 0 || last <= 0) return {{0, rows}};
   const int64_t mid = rows - first - last;
-  int64_t size = (mid + 2) / 3;
+  int64_t nmid = 3;
+  const int64_t cap_aligned = cap_rows - cap_rows % kRowAlign;  // whole tiles per block
+  if (cap_aligned >= kRowAlign && (mid + nmid - 1) / nmid > cap_aligned)
+    nmid = (mid + cap_aligned - 1) / cap_aligned;
+  int64_t size = (mid + nmid - 1) / nmid;
   size += (kRowAlign - size % kRowAlign) % kRowAlign;
+  if (cap_aligned >= kRowAlign && size > cap_aligned) size = cap_aligned;
   std::vector<Block> out{{0, first}};
   for (int64_t r = first; r < rows - last; r += size)
     out.push_back({r, r + size < rows - last ? r + size : rows - last});
@@ -205,9 +239,10 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   const bool wide = dtype == MOA_DTYPE_F32 &&
                     (reduce_code == moa::R_ADD || reduce_code == moa::R_MUL || combine_code == moa::C_MUL ||
                      combine_code == moa::C_DIV);
-  std::vector<Block> blocks = (a_dense && b_dense) ? plan_blocks(rows, rows * N * (int64_t)esz, K)
+  std::vector<Block> blocks = (a_dense && b_dense)
+                                  ? plan_blocks(rows, rows * N * (int64_t)esz, K, (K + N) * (int64_t)esz)
                                                    : std::vector<Block>{{0, rows}};
-  const bool chunked = blocks.size() > 1 && !wide;
+  const bool chunked = blocks.size() > 1 && !wide && K >= 2;
   const auto chunks = chunked ? k_chunks(K, blocks.size() >= 5 ? 8 : (int)blocks.size(), 16)
                               : std::vector<std::pair<int64_t, int64_t>>{{0, K}};
 

@@ -175,3 +175,30 @@ def test_host_entry_argument_errors(rng):
     # surplus worker / empty rows: no work, no error
     _native.product_rows_host(0, res.ctypes.data, a.ctypes.data, b.ctypes.data,
                               3, 4, 3, 4, 3, 3, 2, 0, 5, 1, 0, 0)
+
+
+def test_host_entry_bounded_blocks(monkeypatch, rng):
+    """Every block's A and C rows stay within $MOA_HOST_BLOCK_BYTES (4 GiB by
+    default): a small cap forces many blocks for an outer product (equal
+    blocks) and for a sub-GiB inner product (3/16 first block per k-chunk,
+    extra middle blocks); results bitwise equal one device launch."""
+    torch = _torch()
+    monkeypatch.setenv("MOA_HOST_BLOCK_BYTES", str(3 << 20))  # 3 MiB
+    x, y = rng.random(2000) * 2 - 1, rng.random(700) * 2 - 1
+    res = np.empty(2000 * 700)
+    launch_host(plan_outer((2000,), (700,)), res, x, y, op_pair("subtract", "max"))
+    assert_bits_equal(res, np.subtract.outer(x, y).ravel())
+    for ops, dt in ((moa.MUL_ADD, np.float64), (op_pair("add", "min"), np.float32),
+                    (op_pair("divide", "max"), np.float64)):
+        m, k, n = 2100, 96, 640  # 6.9 MiB of A+C rows: 384-row first block, 128-row last
+        a = (rng.random(m * k) * 100 + 1).astype(dt)
+        b = (rng.random(k * n) * 100 + 1).astype(dt)
+        plan = plan_inner((m, k), (k, n))
+        want = _device_result(plan, np.zeros(m * n, dtype=dt), a, b, ops)
+        for acc in (False, True):
+            res = np.full(m * n, ops.reduce_identity if acc else 0, dtype=dt)
+            pinned = torch.empty(m * n, dtype=torch.from_numpy(res[:1]).dtype,
+                                 pin_memory=True).numpy()
+            pinned[:] = res
+            launch_host(plan, pinned, a, b, ops, accumulate=acc)
+            assert_bits_equal(pinned, want, f"{ops} {dt.__name__} acc={acc}")
