@@ -482,8 +482,19 @@ template <typename T, int C, int R>
 cudaError_t semiring_acc(const Problem& p) {
   constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB || C == C_MUL) &&
                         (R == R_MIN || R == R_MAX);
+  // int32 (add|subtract, min|max): exact integer arithmetic, so the TMA
+  // tropical kernel (64x128 tiles, four-k step) runs it with one DPX
+  // VIADDMNMX per pair and no pre-scan whenever rows are 16-byte aligned
+  constexpr bool i32trop = std::is_same<T, int32_t>::value && (C == C_ADD || C == C_SUB) &&
+                           (R == R_MIN || R == R_MAX);
   if constexpr (cand) {
     return p.accumulate ? tropical_candidate<C, R, true>(p) : tropical_candidate<C, R, false>(p);
+  } else if constexpr (i32trop) {
+    if (tropical_tma_eligible(p))
+      return p.accumulate ? tropical_tma_launch<C, R, 3, true, 3, 1, true, 64>(p, nullptr)
+                          : tropical_tma_launch<C, R, 3, false, 3, 1, true, 64>(p, nullptr);
+    return p.accumulate ? semiring_launch<T, C, R, true, -1>(p, nullptr)
+                        : semiring_launch<T, C, R, false, -1>(p, nullptr);
   } else {
     return p.accumulate ? semiring_launch<T, C, R, true, -1>(p, nullptr)
                         : semiring_launch<T, C, R, false, -1>(p, nullptr);

@@ -59,6 +59,16 @@ __device__ __forceinline__ unsigned long long pair_op_bcast(float x0, float x1, 
         : "=l"(r) : "f"(a), "f"(x0), "f"(x1));
   return r;
 }
+// MODE 3 (int32 data through the same kernel, bit patterns carried as floats):
+// acc = reduce(acc, combine(a, b)) as one DPX add-then-min/max (VIADDMNMX),
+// two's-complement wraparound; subtract adds b's wrapped negation
+template <int C, int R>
+__device__ __forceinline__ float iaddmnmx(float a, float b, float acc) {
+  const int x = __float_as_int(a), y = C == C_SUB ? -__float_as_int(b) : __float_as_int(b);
+  const int z = __float_as_int(acc);
+  return __int_as_float(R == R_MIN ? __viaddmin_s32(x, y, z) : __viaddmax_s32(x, y, z));
+}
+
 __device__ __forceinline__ float lo32(unsigned long long v) { return __uint_as_float((unsigned)v); }
 __device__ __forceinline__ float hi32(unsigned long long v) {
   return __uint_as_float((unsigned)(v >> 32));
@@ -70,11 +80,12 @@ __device__ __forceinline__ float hi32(unsigned long long v) {
 // K >= 1, so the max is unchanged while -inf's sign bit would break the
 // order — or from C's previous contents under MOA_FLAG_ACCUMULATE (whose
 // values the fold mode has already checked).
-template <int R, bool INTFOLD, bool ACC>
+template <int R, bool INTFOLD, bool ACC, bool I32 = false>
 __device__ __forceinline__ void init_acc(float (&acc)[8][8], const float* c, int64_t M, int64_t N,
                                          int64_t ldc, int64_t m0, int64_t n0, int r0, int rstep,
                                          int tx) {
-  const float init = (INTFOLD && R == R_MAX) ? 0.0f : ReduceOp<R>::template identity<float>();
+  const float init = I32 ? __int_as_float(ReduceOp<R>::template identity<int32_t>())
+                     : (INTFOLD && R == R_MAX) ? 0.0f : ReduceOp<R>::template identity<float>();
   // opaque copies of C's origin: otherwise the compiler keeps these addresses
   // and bounds tests alive through the main loop for the epilogue and spills
   if (ACC) asm volatile("" : "+l"(m0), "+l"(n0), "+l"(c));
@@ -273,10 +284,13 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
                         const unsigned* special, int64_t tiles_m, int64_t tiles_n,
                         const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b) {
-  static_assert(MODE == 1 || MODE == 2, "fast modes only");
+  static_assert(MODE == 1 || MODE == 2 || MODE == 3, "fast modes only");
+  static_assert(MODE != 3 || C == C_ADD || C == C_SUB, "int32 mode: add/subtract combines");
   using TT = TropTma<BMT>;
-  constexpr bool INTFOLD = MODE == 2;
-  if (tropical_mode_of<ACC>(C, special) != MODE) return;
+  constexpr bool INTFOLD = MODE == 2, I32 = MODE == 3;
+  if constexpr (!I32) {  // float modes: the device pre-scan picks the fold
+    if (tropical_mode_of<ACC>(C, special) != MODE) return;
+  }
   extern __shared__ __align__(16) unsigned char tt_raw[];
   unsigned char* base = tma::align1k(tt_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + TSTAGES * TT::STAGE_BYTES);
@@ -315,7 +329,7 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
   }
 
   float acc[8][8];
-  init_acc<R, INTFOLD, ACC>(acc, c, M, N, ldc, m0, n0, ty, TT::ROW_STEP, tx);
+  init_acc<R, INTFOLD, ACC, I32>(acc, c, M, N, ldc, m0, n0, ty, TT::ROW_STEP, tx);
 
   for (int64_t kt = 0; kt < KT; kt++) {
     const int stage = (int)(kt % TSTAGES);
@@ -333,11 +347,16 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
         for (int p = 0; p < 2; p++) {
           const float x0 = p ? b0[g].z : b0[g].x, x1 = p ? b0[g].w : b0[g].y;
           const float y0 = p ? b1[g].z : b1[g].x, y1 = p ? b1[g].w : b1[g].y;
-          const unsigned long long s = pair_op_bcast<C>(x0, x1, a0);
-          const unsigned long long t = pair_op_bcast<C>(y0, y1, a1);
           const int j = 4 * g + 2 * p;
-          acc[i][j] = fold3<R, INTFOLD>(acc[i][j], lo32(s), lo32(t));
-          acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], hi32(s), hi32(t));
+          if constexpr (I32) {  // k then k+1, as the exact loop folds them
+            acc[i][j] = iaddmnmx<C, R>(a1, y0, iaddmnmx<C, R>(a0, x0, acc[i][j]));
+            acc[i][j + 1] = iaddmnmx<C, R>(a1, y1, iaddmnmx<C, R>(a0, x1, acc[i][j + 1]));
+          } else {
+            const unsigned long long s = pair_op_bcast<C>(x0, x1, a0);
+            const unsigned long long t = pair_op_bcast<C>(y0, y1, a1);
+            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], lo32(s), lo32(t));
+            acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], hi32(s), hi32(t));
+          }
         }
       }
     };
@@ -398,9 +417,13 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
 #pragma unroll
         for (int g = 0; g < 2; g++)
 #pragma unroll
-          for (int cc = 0; cc < 4; cc++)
-            acc[i][4 * g + cc] =
-                ReduceOp<R>::f(acc[i][4 * g + cc], CombineOp<C>::f(av, bs[k * TBN + 64 * g + cc]));
+          for (int cc = 0; cc < 4; cc++) {
+            if constexpr (I32)
+              acc[i][4 * g + cc] = iaddmnmx<C, R>(av, bs[k * TBN + 64 * g + cc], acc[i][4 * g + cc]);
+            else
+              acc[i][4 * g + cc] = ReduceOp<R>::f(acc[i][4 * g + cc],
+                                                  CombineOp<C>::f(av, bs[k * TBN + 64 * g + cc]));
+          }
       }
     }
     tma::release_stage(&empty[stage], lane);

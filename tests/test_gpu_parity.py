@@ -17,7 +17,7 @@ import pytest
 import oracle
 import paper_0907_0792_b200 as moa
 from paper_0907_0792_b200 import MoaArray, op_pair
-from paper_0907_0792_b200.kernel import launch, plan_inner, plan_outer
+from paper_0907_0792_b200.kernel import KernelPlan, launch, plan_inner, plan_outer
 from parity import assert_bits_equal, assert_within, sum_tolerance
 
 pytestmark = [pytest.mark.gpu, pytest.mark.filterwarnings("ignore::RuntimeWarning")]
@@ -896,6 +896,39 @@ def test_integer_tropical_wraps(rng):
             got = moa.inner(MoaArray((m, k), a.ravel(), dtype=dt), MoaArray((k, n), b.ravel(), dtype=dt),
                             op_pair(comb, red)).data.reshape(m, n)
             np.testing.assert_array_equal(got, want, err_msg=f"{np.dtype(dt).name} {comb}/{red}")
+
+
+@pytest.mark.parametrize("k,lstride", [(68, 68), (67, 68), (130, 132)])
+def test_int32_tropical_tma_route_wraps(k, lstride, rng):
+    """int32 (add|subtract, min|max) with 16-byte aligned rows runs the TMA
+    tropical kernel (one VIADDMNMX per pair, four-k step, pair and lone-k
+    tails when K is odd): full-range values, two's-complement wrap before the
+    fold, write-only and accumulate, bitwise vs numpy."""
+    torch = _torch()
+    m, n = 300, 260
+    info = np.iinfo(np.int32)
+    a = rng.integers(info.min, info.max, size=(m, lstride), endpoint=True, dtype=np.int64).astype(np.int32)
+    b = rng.integers(info.min, info.max, size=(k, n), endpoint=True, dtype=np.int64).astype(np.int32)
+    a[0, :4] = [info.max, info.min, 0, -1]
+    b[:4, 0] = [info.max, info.min, 1, info.min]
+    plan = KernelPlan("inner", m, k, n, lstride, n, n, (m, n))
+    ad, bd = _dev(a.ravel()), _dev(b.ravel())
+    for comb, red in (("add", "min"), ("add", "max"), ("subtract", "min"), ("subtract", "max")):
+        with np.errstate(over="ignore"):
+            s3 = (a[:, :k, None] + b[None, :, :]) if comb == "add" else (a[:, :k, None] - b[None, :, :])
+        want = s3.min(axis=1) if red == "min" else s3.max(axis=1)
+        res = torch.empty(m * n, dtype=torch.int32, device="cuda")
+        launch(plan, res, ad, bd, op_pair(comb, red))
+        np.testing.assert_array_equal(res.cpu().numpy().reshape(m, n), want,
+                                      err_msg=f"{comb}/{red} k={k}")
+        # accumulate: fold into previous contents (the exact loop's semantics)
+        init = rng.integers(info.min, info.max, size=(m, n), endpoint=True,
+                            dtype=np.int64).astype(np.int32)
+        res = _dev(init.ravel().copy())
+        launch(plan, res, ad, bd, op_pair(comb, red), accumulate=True)
+        want_acc = np.minimum(init, want) if red == "min" else np.maximum(init, want)
+        np.testing.assert_array_equal(res.cpu().numpy().reshape(m, n), want_acc,
+                                      err_msg=f"{comb}/{red} k={k} accumulate")
 
 
 @pytest.mark.parametrize("mkn", [(700, 1000, 520),    # cp.async kernels
