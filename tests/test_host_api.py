@@ -317,3 +317,35 @@ def test_k_chunks_align_to_the_dmma_slab():
             assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
             assert all(k0 % 16 == 0 for k0, _ in ch)
             assert len(ch) <= max(1, n)
+
+
+def test_launch_host_validates_before_the_abi():
+    """kernel.launch_host (the host-buffer C ABI from Python) refuses what the
+    raw pointers cannot express — mixed dtypes, non-flat or non-contiguous
+    buffers, a read-only result, buffers shorter than the rows addressed,
+    custom callables — before any native call (so this runs without a GPU)."""
+    import numpy as np
+    import pytest
+
+    from paper_0907_0792_b200 import OpPair, op_pair
+    from paper_0907_0792_b200.kernel import launch_host, plan_inner
+    plan = plan_inner((4, 3), (3, 5))
+    a, b, res = np.zeros(12), np.zeros(15), np.zeros(20)
+    ops = op_pair("add", "min")
+    with pytest.raises(TypeError):
+        launch_host(plan, res, a.astype(np.float32), b, ops)
+    with pytest.raises(ValueError, match="flat"):
+        launch_host(plan, res.reshape(4, 5), a, b, ops)
+    with pytest.raises(ValueError, match="flat"):
+        launch_host(plan, res, np.zeros(24)[::2], b, ops)
+    ro = np.zeros(20)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError, match="writeable"):
+        launch_host(plan, ro, a, b, ops)
+    with pytest.raises(ValueError, match="holds"):
+        launch_host(plan, np.zeros(19), a, b, ops)
+    with pytest.raises(ValueError, match="holds"):
+        launch_host(plan, res, np.zeros(11), b, ops)
+    custom = OpPair(lambda x, y: x, lambda x, y: y, 0.0)
+    with pytest.raises(ValueError, match="custom"):
+        launch_host(plan, res, a, b, custom)
