@@ -138,7 +138,10 @@ uint64_t moa_launch_count(void);
 
 /*
  * Which kernel moa_product_rows would run for these arguments, as a static
- * string ("outer", "fill", "dmma", "semiring_exact", "semiring_fast", "none").
+ * string ("outer", "fill", "dmma", "semiring_exact", "semiring_fast",
+ * "semiring_dpx", "none").  "semiring_dpx": int32 (add|subtract) x (min|max),
+ * exact, on the TMA tropical kernel with one DPX add-then-min/max per pair
+ * when rows are 16-byte aligned (else the exact loop).
  * Host-only; launches nothing.  "semiring_fast" (float32 (add|subtract|
  * multiply) x (min|max), with or without MOA_FLAG_ACCUMULATE) means the
  * kernels that decide on the device, after a NaN/+-0/inf/sign pre-scan of the

@@ -33,7 +33,7 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
-enum class Route { None, Fill, Outer, Dmma, SemiringExact, SemiringFast };
+enum class Route { None, Fill, Outer, Dmma, SemiringExact, SemiringFast, SemiringDpx };
 
 Route route(int dtype, int64_t rows, int64_t K, int64_t N, int comb, int red, uint32_t flags) {
   if (rows <= 0 || N <= 0) return Route::None;
@@ -43,6 +43,9 @@ Route route(int dtype, int64_t rows, int64_t K, int64_t N, int comb, int red, ui
   if (dtype == MOA_DTYPE_F64 && comb == moa::C_MUL && red == moa::R_ADD && !(flags & MOA_FLAG_EXACT))
     return Route::Dmma;
   if (moa::semiring_fast_candidate(dtype, comb, red, acc)) return Route::SemiringFast;
+  if (dtype == MOA_DTYPE_I32 && (comb == moa::C_ADD || comb == moa::C_SUB) &&
+      (red == moa::R_MIN || red == moa::R_MAX))
+    return Route::SemiringDpx;
   return Route::SemiringExact;
 }
 
@@ -53,6 +56,7 @@ const char* route_name(Route r) {
     case Route::Dmma: return "dmma";
     case Route::SemiringExact: return "semiring_exact";
     case Route::SemiringFast: return "semiring_fast";
+    case Route::SemiringDpx: return "semiring_dpx";
     default: return "none";
   }
 }

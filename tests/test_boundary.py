@@ -60,6 +60,7 @@ def test_kernel_routing():
     assert pk(1, 16384, 16384, 16384, 2, 0) == "semiring_exact"  # f32 sums run in f64
     assert pk(1, 16384, 16384, 16384, 2, 3) == "semiring_fast"  # max-times (scanned)
     assert pk(2, 16384, 16384, 16384, 2, 0) == "semiring_exact"  # int32: exact integer fold
+    assert pk(2, 16384, 16384, 16384, 1, 3) == "semiring_dpx"  # int32 tropical: DPX on TMA tiles
     assert pk(3, 16384, 16384, 16384, 0, 2) == "semiring_exact"  # int64 tropical
     assert pk(2, 65536, 1, 2048, 2, 0) == "outer"
     assert pk(0, 65536, 1, 2048, 2, 0) == "outer"
