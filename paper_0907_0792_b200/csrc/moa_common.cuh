@@ -289,17 +289,23 @@ __host__ __device__ inline int tropical_fold_mode(int combine, unsigned fa, unsi
 }
 
 // With MOA_FLAG_ACCUMULATE the result's previous contents are folded too:
-// they must hold no NaN or -0.0 for any fast mode (fc = C's scan flags) and
-// be sign-clear for the unsigned-order fold.
-__host__ __device__ inline int tropical_fold_mode_acc(int combine, unsigned fa, unsigned fb,
-                                                      unsigned fc) {
+// they must hold no NaN or -0.0 for any fast mode (fc = C's scan flags).  The
+// unsigned-order fold also needs sign-clear seeds, except for max: there every
+// combine result is >= +0 and K >= 1, so a negative seed (the -inf identity
+// the reference prefills, say) never wins and is replaced by +0 (init_acc).
+// A min fold with negative seeds drops to FMNMX3 for add/subtract and to the
+// exact loop for multiply, which has no FMNMX3 kernel.
+__host__ __device__ inline int tropical_fold_mode_acc(int combine, int reduce, unsigned fa,
+                                                      unsigned fb, unsigned fc) {
   const int m = tropical_fold_mode(combine, fa, fb);
   if (fc & (S_NAN | S_NZERO)) return 0;
-  return (m == 2 && (fc & S_NEG)) ? 1 : m;
+  if (m == 2 && (fc & S_NEG) && reduce != R_MAX) return combine == C_MUL ? 0 : 1;
+  return m;
 }
 template <bool ACC>
-__device__ __forceinline__ int tropical_mode_of(int combine, const unsigned* special) {
-  return ACC ? tropical_fold_mode_acc(combine, __ldg(special), __ldg(special + 1), __ldg(special + 2))
+__device__ __forceinline__ int tropical_mode_of(int combine, int reduce, const unsigned* special) {
+  return ACC ? tropical_fold_mode_acc(combine, reduce, __ldg(special), __ldg(special + 1),
+                                      __ldg(special + 2))
              : tropical_fold_mode(combine, __ldg(special), __ldg(special + 1));
 }
 

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(SNT, MINB)
   constexpr int STAGES = Shape::STAGES, BM = Shape::BM, BN = Shape::BN;
   constexpr int BK = Shape::BK, KP = Shape::KP;
   if constexpr (MODEK >= 0) {
-    if (tropical_mode_of<ACC>(C, special) != MODEK) return;
+    if (tropical_mode_of<ACC>(C, R, special) != MODEK) return;
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KPair<T>* As = reinterpret_cast<KPair<T>*>(smem_raw);

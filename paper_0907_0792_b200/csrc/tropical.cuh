@@ -96,7 +96,11 @@ __device__ __forceinline__ void init_acc(float (&acc)[8][8], const float* c, int
       acc[i][j] = init;
       if (ACC) {
         const int64_t row = m0 + r0 + rstep * i, col = n0 + 64 * (j >> 2) + 4 * tx + (j & 3);
-        if (row < M && col < N) acc[i][j] = c[row * ldc + col];
+        if (row < M && col < N) {
+          const float v = c[row * ldc + col];
+          // unsigned-order max: a negative seed never wins against results >= +0
+          acc[i][j] = (INTFOLD && !I32 && R == R_MAX && (__float_as_uint(v) >> 31)) ? 0.0f : v;
+        }
       }
     }
 }
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(TNT, 2)
                     const unsigned* special, int64_t tiles_m, int64_t tiles_n) {
   static_assert(MODE == 1 || MODE == 2, "fast modes only");
   constexpr bool INTFOLD = MODE == 2;
-  if (tropical_mode_of<ACC>(C, special) != MODE) return;
+  if (tropical_mode_of<ACC>(C, R, special) != MODE) return;
   extern __shared__ __align__(16) float tsm[];
   float* As = tsm;
   float* Bs = tsm + TSTAGES * TA_STAGE;
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
   using TT = TropTma<BMT>;
   constexpr bool INTFOLD = MODE == 2, I32 = MODE == 3;
   if constexpr (!I32) {  // float modes: the device pre-scan picks the fold
-    if (tropical_mode_of<ACC>(C, special) != MODE) return;
+    if (tropical_mode_of<ACC>(C, R, special) != MODE) return;
   }
   extern __shared__ __align__(16) unsigned char tt_raw[];
   unsigned char* base = tma::align1k(tt_raw);

@@ -502,6 +502,35 @@ def test_tropical_fast_and_exact_loops_agree(dt, mkn, rng):
 
 
 @pytest.mark.parametrize("mkn", [(300, 132, 260), (257, 131, 300)])  # TMA / cp.async kernels
+def test_tropical_accumulate_seeds(mkn, rng):
+    """float32 (add|subtract|multiply, min|max) under MOA_FLAG_ACCUMULATE with
+    the reference's identity prefill (+-inf), with negative and with mixed
+    seeds: the unsigned-order max fold replaces negative seeds by +0 (they can
+    never win against results >= +0), a min fold with negative seeds leaves
+    the fast loop (multiply has no FMNMX3 kernel: it once ran nothing and left
+    the -inf prefill in place).  Bitwise vs the reference's fold from res."""
+    torch = _torch()
+    m, k, n = mkn
+    a = (rng.random(m * k) * 100).astype(np.float32)
+    b = (rng.random(k * n) * 100).astype(np.float32)
+    ad, bd = _dev(a), _dev(b)
+    plan = plan_inner((m, k), (k, n))
+    for comb in ("add", "subtract", "multiply"):
+        for red in ("min", "max"):
+            ops = op_pair(comb, red)
+            c, r = ops.codes()
+            seeds = {"identity": np.full(m * n, ops.reduce_identity, dtype=np.float32),
+                     "negative": -(rng.random(m * n) * 50).astype(np.float32) - 1,
+                     "mixed": ((rng.random(m * n) - 0.5) * 20000).astype(np.float32)}
+            for name, seed in seeds.items():
+                res = _dev(seed.copy())
+                launch(plan, res, ad, bd, ops, accumulate=True)
+                want = oracle.product(a, b, m, k, n, c, r,
+                                      res=seed.astype(np.float64)).astype(np.float32)
+                assert_bits_equal(res.cpu().numpy(), want, f"{ops} seed={name}")
+
+
+@pytest.mark.parametrize("mkn", [(300, 132, 260), (257, 131, 300)])  # TMA / cp.async kernels
 def test_max_times_fast_fold(mkn, rng):
     """float32 (multiply, min|max): non-negative data runs the FMUL2 +
     unsigned-order fold; zeros with infinities (0 x inf = NaN), negative
