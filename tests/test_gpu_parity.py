@@ -501,6 +501,38 @@ def test_tropical_fast_and_exact_loops_agree(dt, mkn, rng):
                 assert_bits_equal(got, want, f"{ops} poison={poison}")
 
 
+def _identity(ops, dt):
+    if np.dtype(dt).kind == "f":
+        return ops.reduce_identity
+    info = np.iinfo(dt)
+    return {"add": 0, "multiply": 1, "min": info.max, "max": info.min}[ops.reduce_name]
+
+
+@pytest.mark.parametrize("mkn", [(200, 132, 260), (130, 67, 97)])  # aligned / unaligned
+def test_accumulate_from_identity_equals_write_only_every_route(mkn, rng):
+    """The reference's contract for its loop (kernel.py:149 + _ckernel.pyx:51,70):
+    folding into a result prefilled with the reduce identity gives the same
+    bits as the write-only launch — for all 24 (combine, reduce) pairs on
+    every dtype, through every kernel route (TMA and cp.async tiles, fast and
+    exact folds, DPX, division)."""
+    torch = _torch()
+    m, k, n = mkn
+    plan = plan_inner((m, k), (k, n))
+    for dt in (np.float64, np.float32, np.int32, np.int64):
+        if np.dtype(dt).kind == "f":
+            a, b = (rng.random(m * k) * 9 + 0.5).astype(dt), (rng.random(k * n) * 9 + 0.5).astype(dt)
+        else:
+            a, b = rng.integers(1, 9, m * k).astype(dt), rng.integers(1, 9, k * n).astype(dt)
+        ad, bd = _dev(a), _dev(b)
+        for ops in moa.builtin_pairs():
+            w = torch.empty(m * n, dtype=ad.dtype, device="cuda")
+            launch(plan, w, ad, bd, ops)
+            acc = torch.full((m * n,), _identity(ops, dt), dtype=ad.dtype, device="cuda")
+            launch(plan, acc, ad, bd, ops, accumulate=True)
+            assert_bits_equal(acc.cpu().numpy(), w.cpu().numpy(),
+                              f"{np.dtype(dt).name} {ops} {mkn}")
+
+
 @pytest.mark.parametrize("mkn", [(300, 132, 260), (257, 131, 300)])  # TMA / cp.async kernels
 def test_tropical_accumulate_seeds(mkn, rng):
     """float32 (add|subtract|multiply, min|max) under MOA_FLAG_ACCUMULATE with
