@@ -533,6 +533,37 @@ def test_accumulate_from_identity_equals_write_only_every_route(mkn, rng):
                               f"{np.dtype(dt).name} {ops} {mkn}")
 
 
+@pytest.mark.parametrize("mkn", [(200, 132, 260), (130, 67, 97)])
+def test_row_sets_equal_full_launch_every_route(mkn, rng):
+    """execute_parallel's determinism (tests/test_acceptance.py:84-103 of the
+    reference): the rows 0::2 and 1::2 launched separately, and a contiguous
+    row block launched as its own product, give the bits of one full launch —
+    for all 24 pairs on every dtype (so sharding rows over workers or GPUs
+    never changes a result)."""
+    torch = _torch()
+    m, k, n = mkn
+    plan = plan_inner((m, k), (k, n))
+    r0, r1 = m // 3, m // 3 + 64
+    for dt in (np.float64, np.float32, np.int32, np.int64):
+        if np.dtype(dt).kind == "f":
+            a, b = (rng.random(m * k) * 9 + 0.5).astype(dt), (rng.random(k * n) * 9 + 0.5).astype(dt)
+        else:
+            a, b = rng.integers(1, 9, m * k).astype(dt), rng.integers(1, 9, k * n).astype(dt)
+        ad, bd = _dev(a), _dev(b)
+        for ops in moa.builtin_pairs():
+            full = torch.empty(m * n, dtype=ad.dtype, device="cuda")
+            launch(plan, full, ad, bd, ops)
+            parts = torch.empty_like(full)
+            launch(plan, parts, ad, bd, ops, start=0, step=2)
+            launch(plan, parts, ad, bd, ops, start=1, step=2)
+            assert_bits_equal(parts.cpu().numpy(), full.cpu().numpy(),
+                              f"{np.dtype(dt).name} {ops} rows k::2")
+            blk = torch.empty((r1 - r0) * n, dtype=ad.dtype, device="cuda")
+            launch(plan_inner((r1 - r0, k), (k, n)), blk, ad[r0 * k:r1 * k], bd, ops)
+            assert_bits_equal(blk.cpu().numpy(), full[r0 * n:r1 * n].cpu().numpy(),
+                              f"{np.dtype(dt).name} {ops} rows {r0}:{r1}")
+
+
 @pytest.mark.parametrize("mkn", [(300, 132, 260), (257, 131, 300)])  # TMA / cp.async kernels
 def test_tropical_accumulate_seeds(mkn, rng):
     """float32 (add|subtract|multiply, min|max) under MOA_FLAG_ACCUMULATE with
