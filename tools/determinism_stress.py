@@ -18,10 +18,18 @@ cases = [  # (label, dtype, ops, (m, k, n), shift: 1 = misaligned A -> cp.async 
     ("int32 DPX TMA", np.int32, op_pair("add", "min"), (2048, 512, 4096), 0),
     ("f64 exact (add,min)", np.float64, op_pair("add", "min"), (1024, 256, 1024), 0),
     ("f32 max-times", np.float32, op_pair("multiply", "max"), (2048, 256, 2048), 0),
+    ("f32 (divide,max) exact", np.float32, op_pair("divide", "max"), (1024, 256, 1024), 0),
+    ("f64 (max,multiply)", np.float64, op_pair("max", "multiply"), (1024, 256, 1024), 0),
+    ("f32 (min,min) exact", np.float32, op_pair("min", "min"), (1024, 256, 1024), 0),
+    ("int32 (multiply,add)", np.int32, op_pair("multiply", "add"), (1024, 256, 1024), 0),
+    ("int32 DPX cp.async", np.int32, op_pair("subtract", "max"), (1024, 255, 1024), 1),
+    ("int64 (add,min)", np.int64, op_pair("add", "min"), (1024, 256, 1024), 0),
+    ("f64 (divide,add)", np.float64, op_pair("divide", "add"), (1024, 256, 1024), 0),
 ]
-torch_dt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32}
+torch_dt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32,
+            np.int64: torch.int64}
 for label, dt, ops, (m, k, n), shift in cases:
-    if dt == np.int32:
+    if np.dtype(dt).kind == "i":
         a = rng.integers(-1000, 1000, m * k + 1).astype(dt); b = rng.integers(-1000, 1000, k * n).astype(dt)
     else:
         a = (rng.random(m * k + 1) * 100).astype(dt); b = (rng.random(k * n) * 100).astype(dt)
@@ -33,10 +41,17 @@ for label, dt, ops, (m, k, n), shift in cases:
     c = torch.empty_like(first)
     for r in range(reps):
         launch(plan, c, ad, bd, ops)
-        bad_w += int(not torch.equal(c.view(torch.uint8) if dt != np.int32 else c, first.view(torch.uint8) if dt != np.int32 else first))
-        c.fill_(ops.reduce_identity if dt != np.int32 else (2**31 - 1 if ops.reduce_name == "min" else -2**31))
+        isint = np.dtype(dt).kind == "i"
+        bad_w += int(not torch.equal(c if isint else c.view(torch.uint8),
+                                     first if isint else first.view(torch.uint8)))
+        if isint:
+            info = np.iinfo(dt)
+            c.fill_({"add": 0, "multiply": 1, "min": int(info.max), "max": int(info.min)}[ops.reduce_name])
+        else:
+            c.fill_(ops.reduce_identity)
         launch(plan, c, ad, bd, ops, accumulate=True)
-        bad_a += int(not torch.equal(c, first))
+        bad_a += int(not torch.equal(c if isint else c.view(torch.uint8),
+                                     first if isint else first.view(torch.uint8)))
     print(f"{label:24s} {m}x{k}x{n}: {reps} write-only launches differing {bad_w}, "
           f"{reps} accumulate launches differing {bad_a}", flush=True)
 x = torch.from_numpy(rng.random(65536)).cuda(); y = torch.from_numpy(rng.random(2048)).cuda()
