@@ -202,3 +202,10 @@ def test_host_entry_bounded_blocks(monkeypatch, rng):
             pinned[:] = res
             launch_host(plan, pinned, a, b, ops, accumulate=acc)
             assert_bits_equal(pinned, want, f"{ops} {dt.__name__} acc={acc}")
+        # a strided row set (rows 1, 3, 5, ...) through the same multi-block
+        # schedule: A rows and result rows move by 2-D copies
+        res = np.full(m * n, 5, dtype=dt)
+        launch_host(plan, res, a, b, ops, start=1, step=2)
+        got, ref = res.reshape(m, n), want.reshape(m, n)
+        assert_bits_equal(got[1::2].ravel(), ref[1::2].ravel(), f"{ops} {dt.__name__} rows 1::2")
+        assert np.all(got[0::2] == 5)
