@@ -48,3 +48,29 @@ def test_reference_arm_line():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "0")
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_multi_rank_line_over_gloo():
+    """The N>1 code path the driver's scaling run takes (torchrun, one JSON
+    line from rank 0, max over ranks), exercised with two ranks sharing the
+    test box's GPU over gloo (timings meaningless there; NCCL needs one GPU
+    per rank): weak c2 with B broadcast once, strong c4/c5 legs with the
+    k-chunked broadcast inside every step."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "2",
+                          "--warmup", "3", "--dist-backend", "gloo", "--no-cpu"],
+                         cwd=REPO, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert REQUIRED <= d.keys() and d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert "once, before the timed region" in d["config"]["parallelism"]
+    assert set(d["inner"]) == {"c4", "c5"}
+    for leg in d["inner"].values():
+        assert leg["scaling"] == "strong" and leg["rows_per_rank"] == 8192 and leg["value"] > 0
