@@ -58,15 +58,19 @@ METRIC = {"c2": ("outer-product GB/s", "GB/s"),
           "c4": ("inner-product GFLOP/s", "GFLOP/s"),
           "c5": ("tropical inner-product G pairs/s", "Gpairs/s")}
 SCALING = {"c2": "weak", "c1": "weak", "c3": "weak", "c4": "strong", "c5": "strong"}
-FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
+SM_COUNT = 148
 
 
 # ---------------------------------------------------------------------------- peaks
-def hbm_peak() -> tuple[float, str]:
+# Every roofline denominator is a MEASURED figure read from a committed file;
+# a missing file leaves the figure unmeasured (peak/frac null) instead of
+# falling back to a hard-coded number.  The theoretical ceiling of the same
+# pipe at the run's SM clock is printed beside each one.
+def hbm_peak() -> tuple[float | None, str]:
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
         return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
-    return FALLBACK_HBM_GBS, "B200_PROFILING.md fallback"
+    return None, "unmeasured: MEASURED_PEAKS.json absent"
 
 
 def microbench_peaks() -> dict:
@@ -74,15 +78,14 @@ def microbench_peaks() -> dict:
     return json.loads(p.read_text()) if p.exists() else {}
 
 
-def fp64_peak() -> tuple[float, str]:
-    mb = microbench_peaks()
-    vals = [v for k, v in mb.items() if k.startswith("dmma_")]
+def fp64_peak() -> tuple[float | None, str]:
+    vals = [v for k, v in microbench_peaks().items() if k.startswith("dmma_")]
     if vals:
         return max(vals), "measured DMMA mma.sync f64 microbenchmark (profiles/r01_peaks_microbench.json)"
-    return 36.96, "measured DMMA microbenchmark (r01)"
+    return None, "unmeasured: profiles/r01_peaks_microbench.json absent"
 
 
-def minplus_peak() -> tuple[float, str]:
+def minplus_peak() -> tuple[float | None, str]:
     """Best measured (add, min) pair rate on the ALU/FMA pipes, G pairs/s.
 
     profiles/r01_minplus_mix2.json holds warp-instructions per clock per SM for
@@ -92,10 +95,26 @@ def minplus_peak() -> tuple[float, str]:
         mix = json.loads(p.read_text())
         units = max(mix.get("fadd2_fmnmx3_pairs_winstr_per_clk_sm", 0.0),
                     mix.get("fadd2_vimnmx3_units_winstr_per_clk_sm", 0.0))
-        return (units * 64 * 148 * 1.965e9 / 1e9,
+        return (units * 64 * SM_COUNT * 1.965e9 / 1e9,
                 "measured FADD2+VIMNMX3 / FADD2+FMNMX3 instruction-mix microbenchmark "
                 "(profiles/r01_minplus_mix2.json), best mix, 1965 MHz")
-    return 24470.0, "measured FADD2+VIMNMX3 microbenchmark (r01)"
+    return None, "unmeasured: profiles/r01_minplus_mix2.json absent"
+
+
+def theoretical(key: str, sm_mhz: float | None) -> dict:
+    """The pipe's nominal ceiling at the run's SM clock (max clock if unsampled)."""
+    mhz = sm_mhz or 1965.0
+    if key == "c5":
+        # one FADD2 + one 3-input min per two pairs: 1 warp-instruction per
+        # 32 pairs, 4 issue slots per SM per clock
+        return {"value": round(SM_COUNT * 4 * 32 * mhz * 1e6 / 1e9, 1), "unit": "Gpairs/s",
+                "what": "issue limit: 1 instruction per pair per lane (FADD2 + 3-input min "
+                        "per 2 pairs), 4 schedulers x 32 lanes x 148 SMs", "sm_mhz": mhz}
+    if key == "c2":
+        return {"value": None, "unit": "GB/s", "what": "write-only ceiling measured: cudaMemset "
+                f"{microbench_peaks().get('memset_GBs')} GB/s (profiles/r01_peaks_microbench.json)"}
+    return {"value": round(SM_COUNT * 64 * 2 * mhz * 1e6 / 1e12, 2), "unit": "TFLOP/s",
+            "what": "148 SMs x 64 FP64 FMA/clk (DMMA) x 2 flop", "sm_mhz": mhz}
 
 
 def ncu_traffic(workload: str):
@@ -340,29 +359,35 @@ def measure_device(w, rows_range, a_host, b_host, steps, warmup, device, world, 
             "graph": graph is not None}
 
 
-def roofline(w, rows: int, kernel_ms: float) -> dict:
+def roofline(w, rows: int, kernel_ms: float, sm_mhz: float | None = None) -> dict:
     m, k, n = w.mkn
     if w.key == "c2":
         algo = unit_amount(w, rows)
         peak, src = hbm_peak()
         achieved = algo / (kernel_ms * 1e-3) / 1e9
-        return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(w.key),
-                "algorithmic_bytes_per_launch": int(algo), "peak_source": src}
-    if w.key == "c5":
-        pairs = rows * k * n
+        out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+               "algorithmic_bytes_per_launch": int(algo)}
+    elif w.key == "c5":
+        algo = rows * k * n
         peak, src = minplus_peak()
-        achieved = pairs / (kernel_ms * 1e-3) / 1e9
-        return {"bound": "alu", "achieved": round(achieved, 1), "peak": round(peak, 1),
-                "unit": "Gpairs/s", "frac": round(achieved / peak, 4),
-                "traffic": ncu_traffic(w.key), "algorithmic_pairs_per_launch": pairs,
-                "peak_source": src}
-    flops = 2.0 * rows * k * n
-    peak, src = fp64_peak()
-    achieved = flops / (kernel_ms * 1e-3) / 1e12
-    return {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(w.key),
-            "algorithmic_flops_per_launch": int(flops), "peak_source": src}
+        achieved = algo / (kernel_ms * 1e-3) / 1e9
+        out = {"bound": "alu", "achieved": round(achieved, 1),
+               "peak": None if peak is None else round(peak, 1), "unit": "Gpairs/s",
+               "algorithmic_pairs_per_launch": algo}
+    else:
+        algo = 2.0 * rows * k * n
+        peak, src = fp64_peak()
+        achieved = algo / (kernel_ms * 1e-3) / 1e12
+        out = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+               "algorithmic_flops_per_launch": int(algo)}
+    out["frac"] = None if peak is None else round(achieved / peak, 4)
+    out["traffic"] = ncu_traffic(w.key)
+    out["peak_source"] = src
+    out["theoretical"] = theoretical(w.key, sm_mhz)
+    th = out["theoretical"]["value"]
+    if th:
+        out["frac_of_theoretical"] = round(achieved / th, 4)
+    return out
 
 
 # ---------------------------------------------------------------------------- e2e leg
@@ -441,78 +466,193 @@ def measure_e2e_cabi(w, a_pin, b_pin, steps, warmup, device):
     return elapsed
 
 
-# ---------------------------------------------------------------------------- CPU legs
-def cpu_reference_time(w, a, b, budget_s: float = 10.0, max_reps: int = 500, rows: int | None = None,
-                       min_reps: int = 3):
-    """Reference hot loop (oracle/_ref, else the C port) on all host cores.
+def measure_e2e_pageable(w, a, b, steps, warmup):
+    """The public API exactly as a reference user calls it: ``MoaArray`` built
+    from ordinary (pageable) numpy arrays, ``moa.outer``/``moa.inner``, the
+    result handed back in host memory; returns seconds for ``steps`` calls."""
+    import paper_0907_0792_b200 as moa
+    from paper_0907_0792_b200 import MoaArray
+    A = MoaArray(w.shape_a, a, dtype=w.dtype)
+    B = MoaArray(w.shape_b, b, dtype=w.dtype)
+    fn = moa.inner if w.mode == "inner" else moa.outer
+    t_first = time.perf_counter()
+    out = fn(A, B, w.ops)
+    t_first = time.perf_counter() - t_first
+    for _ in range(max(0, warmup - 1)):
+        out = None
+        out = fn(A, B, w.ops)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = None
+        out = fn(A, B, w.ops)
+    elapsed = time.perf_counter() - t0
+    del out
+    return elapsed, t_first
 
-    Returns (seconds per unit of ``rows`` rows, kind, cores, sample description)."""
+
+# ---------------------------------------------------------------------------- CPU legs
+def cpu_rows_for(w, cores: int) -> int:
+    """configs 1-3 in full; configs 4-5 on R = 32*W contiguous
+    rows (W = the host's cores), extrapolated x M/R (the per-row cost is constant)."""
+    m = w.mkn[0]
+    return m if w.key in ("c1", "c2", "c3") else min(m, 32 * cores)
+
+
+def _cpu_runner(w, a, b, rows):
+    """One call of the reference's execute_parallel on the first ``rows`` rows:
+    an identity-filled result (kernel.py:149) and W threads, worker k running
+    product_rows(..., start=k, step=W) (parallel.py:37-43), through the
+    reference's own compiled loop (oracle/_ref) or, if absent, the C port.
+    Inputs are float64 before the clock starts, as the reference's bench
+    builds its MoaArrays outside the timer (bench.py:110-111)."""
     import oracle
     m, k, n = w.mkn
     cores = oracle.host_cores()
-    rows = m if rows is None else rows
-    a_s = a[:rows * (k if w.mode == "inner" else 1)]
+    a_s = np.ascontiguousarray(a[:rows * (k if w.mode == "inner" else 1)], dtype=np.float64)
+    b64 = np.ascontiguousarray(b, dtype=np.float64)
     comb, red = w.ops.codes()
     kind = "reference" if oracle.ref_kernel() is not None else "port"
-    run = (lambda: oracle.reference_product(a_s, b, rows, k, n, comb, red, workers=cores)) \
-        if kind == "reference" else \
-        (lambda: oracle.product(a_s, b, rows, k, n, comb, red, workers=cores))
+    fn = oracle.reference_product if kind == "reference" else oracle.product
+
+    def run():
+        fn(a_s, b64, rows, k, n, comb, red, workers=cores)
+    return run, kind, cores
+
+
+def cpu_reference_time(w, a, b, rows: int, reps: int = 3) -> dict:
+    """Best of ``reps`` timed calls (bench.py:118-133 protocol, best instead of
+    mean as SURVEY.md §8(d) asks); returns the cpu_baseline object."""
+    m = w.mkn[0]
+    run, kind, cores = _cpu_runner(w, a, b, rows)
     times = []
-    t_end = time.perf_counter() + budget_s
-    while len(times) < max_reps and (len(times) < min_reps or time.perf_counter() < t_end):
+    for _ in range(reps):
         t0 = time.perf_counter()
         run()
         times.append(time.perf_counter() - t0)
-    sample = (f"{rows} of {m} result rows (full K={k}, N={n}), {len(times)} reps, median; "
-              f"identity prefill + product_rows over {cores} threads, round-robin rows "
-              f"(reference parallel.py:37-43); inputs {'float32 upcast to float64' if w.dtype == np.float32 else 'float64'}")
-    return statistics.median(times), kind, cores, sample, rows
+    best = min(times)
+    sample = (f"W={cores} threads, R={rows} of M={m} contiguous result rows (full K, N)"
+              + ("" if rows == m else f", extrapolated x M/R = x{m / rows:g}")
+              + f"; best of {reps} ({', '.join(f'{t:.3f}' for t in times)} s); identity "
+              f"prefill + product_rows(start=k, step=W) per thread (reference "
+              f"parallel.py:37-43); inputs "
+              + ("float32 upcast to float64 before the clock" if w.dtype == np.float32
+                 else "float64"))
+    metric, unit = METRIC[w.key]
+    return {"value": round(to_unit(w, unit_amount(w, rows), best), 4), "unit": unit,
+            "cores": cores, "kind": kind, "sample": sample, "seconds_per_sample": best}
 
 
-def cpu_rows_for(w) -> int:
+def job_config(w, world: int) -> dict:
+    """The workload's description, identical on both arms (``--impl ours`` and
+    ``--impl reference``), so the driver compares like with like."""
+    from paper_0907_0792_b200.distributed import row_block
     m, k, n = w.mkn
-    return {"c1": m, "c2": m, "c3": m, "c4": 256, "c5": 256}[w.key]
+    scaling = SCALING[w.key]
+    rows = m if scaling == "weak" else row_block(m, world, 0)[1]
+    return {"workload": f"{w.key}: {w.description}", "M": m, "K": k, "N": n,
+            "ranks": world, "rows_per_rank": rows,
+            "parallelism": ("single GPU" if world == 1 else
+                            f"row-sharded x{world}, B broadcast from rank 0 "
+                            + ("inside every step" if scaling == "strong" else
+                               "once, before the timed region")),
+            "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
 def run_reference(args) -> None:
+    """The reference arm: the reference's own CPU implementation of the path
+    on this box's host cores, on the same workload as ``--impl ours``.  Never
+    loads this repo's CUDA library (tests/test_bench_reference_arm.py)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     w = WORKLOADS[args.config]
     a, b = w.generate()
-    rows = cpu_rows_for(w)
-    m, k, n = w.mkn
     import oracle
-    kind = "reference" if oracle.ref_kernel() is not None else "port"
-    cores = oracle.host_cores()
-    comb, red = w.ops.codes()
-    a_s = a[:rows * (k if w.mode == "inner" else 1)]
-
-    def one():
-        if kind == "reference":
-            oracle.reference_product(a_s, b, rows, k, n, comb, red, workers=cores)
-        else:
-            oracle.product(a_s, b, rows, k, n, comb, red, workers=cores)
+    rows = cpu_rows_for(w, oracle.host_cores())
+    m = w.mkn[0]
+    run, kind, cores = _cpu_runner(w, a, b, rows)
     for _ in range(args.warmup):
-        one()
+        run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        one()
+        run()
     el = time.perf_counter() - t0
-    amount = unit_amount(w, rows)
-    value = to_unit(w, amount * args.steps, el)
+    value = to_unit(w, unit_amount(w, rows) * args.steps, el)
     metric, unit = METRIC[w.key]
+    sample = (f"W={cores} threads, R={rows} of M={m} contiguous result rows per step "
+              "(full K, N)" + ("" if rows == m else f", extrapolated x M/R = x{m / rows:g}"))
     line = {"impl": "reference", "metric": metric, "value": round(value, 4), "unit": unit,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
-            "scaling": SCALING[w.key], "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generators of SURVEY.md §8d)",
-            "config": {"workload": f"{w.key}: {w.description}", "sample_rows": rows},
+            "scaling": SCALING[w.key], "vs_baseline": None,
+            "dtype": "f32" if w.dtype == np.float32 else "f64",
+            "data": "synthetic (seeded generators of SURVEY.md §8d; no public dataset)",
+            "config": job_config(w, args.gpus),
+            "execution": f"reference compiled loop ({kind}, oracle/_ref) on {cores} host "
+                         "threads, rank 0 only; no GPU",
             "cpu_baseline": {"value": round(value, 4), "unit": unit, "cores": cores, "kind": kind,
-                             "sample": f"{rows} of {m} result rows per step (full K, N)"},
+                             "sample": sample},
             "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def inner_leg(key, device, world, rank, group=None) -> dict:
+    """One BASELINE inner config: device-resident value and roofline, and the
+    same product end to end from host buffers (C ABI at N=1; the sharded
+    host path at N>1)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_0907_0792_b200.distributed import row_block
+    wi = WORKLOADS[key]
+    ai, bi = wi.generate()
+    mi, ki, ni = wi.mkn
+    rr = (0, mi) if world == 1 else row_block(mi, world, rank)
+    st = 20 if key in ("c1", "c3") else 3
+    d = measure_device(wi, rr, ai, bi, st, 3, device, world, rank, group)
+    step_ms, kern_ms = d["step_ms_total"], d["kernel_ms_mean"]
+    if world > 1:
+        t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        step_ms, kern_ms = t[0].item(), t[1].item()
+    amt = unit_amount(wi, mi)
+    isz = np.dtype(wi.dtype).itemsize
+    leg = {"metric": METRIC[key][0], "unit": METRIC[key][1], "scaling": SCALING[key],
+           "value": round(to_unit(wi, amt, step_ms / st * 1e-3), 2),
+           "rows_per_rank": rr[1] - rr[0], "kernel_ms": round(kern_ms, 4),
+           "roofline": roofline(wi, rr[1] - rr[0], kern_ms, d["clocks"].get("sm_mhz")),
+           "clocks": d["clocks"], "gpu_launches": d["launches"]}
+    ap, bp = pinned_copy(ai), pinned_copy(bi)
+    e2e_st = 20 if key == "c1" else 3
+    el_i = measure_e2e(wi, rr, ap, bp, e2e_st, 3, device, world, rank, group)
+    if world == 1:
+        el_c = measure_e2e_cabi(wi, ap, bp, e2e_st, 3, device)
+        leg["e2e"] = {"value": round(to_unit(wi, amt * e2e_st, el_c), 2), "unit": METRIC[key][1],
+                      "ms_per_step": round(el_c / e2e_st * 1e3, 3),
+                      "h2d_bytes_per_step": (mi * ki + ki * ni) * isz,
+                      "d2h_bytes_per_step": mi * ni * isz,
+                      "path": "moa_product_rows_host (C ABI) on page-locked host buffers "
+                              "(streamed row blocks)"}
+        leg["e2e_api"] = {"value": round(to_unit(wi, amt * e2e_st, el_i), 2),
+                          "unit": METRIC[key][1], "ms_per_step": round(el_i / e2e_st * 1e3, 3),
+                          "path": "moa.inner on pinned host MoaArrays (streamed row blocks)"}
+        if key == "c4":
+            el_p, first = measure_e2e_pageable(wi, ai, bi, 2, 1)
+            leg["e2e_pageable"] = {"value": round(to_unit(wi, amt * 2, el_p), 2),
+                                   "unit": METRIC[key][1], "ms_per_step": round(el_p / 2 * 1e3, 3),
+                                   "first_call_ms": round(first * 1e3, 1),
+                                   "path": "moa.inner on MoaArray(numpy) (pageable) inputs"}
+    else:
+        leg["e2e"] = {"value": round(to_unit(wi, amt * e2e_st, el_i), 2), "unit": METRIC[key][1],
+                      "ms_per_step": round(el_i / e2e_st * 1e3, 3),
+                      "h2d_bytes_per_step": (mi * ki + ki * ni) * isz,
+                      "d2h_bytes_per_step": mi * ni * isz,
+                      "path": "distributed.sharded_product_host: A rows per rank + B on rank 0 "
+                              "from page-locked host buffers, broadcast, product, result block "
+                              "back to host; max over ranks"}
+    del ap, bp
+    return leg, (ai, bi)
 
 
 # ---------------------------------------------------------------------------- main
@@ -524,9 +664,10 @@ def main() -> None:
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-inner", action="store_true", help="skip the extra inner-product legs")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     ap.add_argument("--legs", nargs="*", default=None,
-                    help="inner-product legs to run beside c2 (default: all of c1 c3 c4 c5)")
+                    help="inner-product legs to run beside c2 (default: c1 c3 c4 c5 at N=1, "
+                         "c4 c5 at N>1)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N>1 (gloo only to exercise the "
                          "multi-rank code path on fewer GPUs than ranks; timings meaningless)")
@@ -554,11 +695,9 @@ def main() -> None:
     a, b = w.generate()
     if scaling == "weak":
         rows_range = (0, m)   # every rank owns one full unit (weak scaling)
-        job_rows = m * world
     else:
         from paper_0907_0792_b200.distributed import row_block
         rows_range = row_block(m, world, rank)
-        job_rows = m
 
     dev = measure_device(w, rows_range, a, b, args.steps, max(args.warmup, 3), device, world, rank)
     step_ms = dev["step_ms_total"]
@@ -574,29 +713,29 @@ def main() -> None:
     else:
         launches = dev["launches"]
     ms_per_step = step_ms / args.steps
-    job_amount = unit_amount(w, job_rows) if scaling == "weak" else unit_amount(w, m)
-    if scaling == "weak":
-        job_amount = unit_amount(w, m) * world
+    job_amount = unit_amount(w, m) * (world if scaling == "weak" else 1)
     value = to_unit(w, job_amount, ms_per_step * 1e-3)
 
-    # e2e through the public API, pinned host buffers
+    # e2e: host buffers, copies inside the clock
     a_pin, b_pin = pinned_copy(a), pinned_copy(b)
     e2e_steps = max(2, min(args.steps, 5))
     el = measure_e2e(w, rows_range, a_pin, b_pin, e2e_steps, 2, device, world, rank)
     isz = np.dtype(w.dtype).itemsize
-    if scaling == "weak":
-        h2d = world * (m * k + k * n) * isz if w.mode == "inner" else world * (m + n) * isz
-        d2h = world * m * n * isz
-    else:
-        h2d = (m * k + k * n) * isz
-        d2h = m * n * isz
+    units = world if scaling == "weak" else 1
+    h2d = units * ((m * k + k * n) if w.mode == "inner" else (m + n)) * isz
+    d2h = units * m * n * isz
     e2e_value = to_unit(w, job_amount * e2e_steps, el)
-    e2e_api = None
+    e2e_api = e2e_pageable = None
     if world == 1:  # headline e2e through the C ABI; the public API beside it
         e2e_api = {"value": round(e2e_value, 3), "unit": METRIC[w.key][1],
                    "path": "moa.outer/inner on pinned host MoaArrays"}
         el = measure_e2e_cabi(w, a_pin, b_pin, e2e_steps, 2, device)
         e2e_value = to_unit(w, job_amount * e2e_steps, el)
+        el_p, first = measure_e2e_pageable(w, a, b, e2e_steps, 2)
+        e2e_pageable = {"value": round(to_unit(w, job_amount * e2e_steps, el_p), 3),
+                        "unit": METRIC[w.key][1], "first_call_ms": round(first * 1e3, 1),
+                        "path": "moa.outer/inner on MoaArray(numpy) (pageable) inputs, "
+                                "result returned as a host MoaArray"}
     del a_pin, b_pin
 
     metric, unit = METRIC[w.key]
@@ -605,103 +744,47 @@ def main() -> None:
             "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32" if w.dtype == np.float32 else "f64",
             "data": "synthetic (seeded generators of SURVEY.md §8d; no public dataset)",
-            "config": {"workload": f"{w.key}: {w.description}", "M": m, "K": k, "N": n,
-                       "rows_per_rank": rows_range[1] - rows_range[0],
-                       "parallelism": ("single GPU" if world == 1 else
-                                       f"row-sharded x{world}, B broadcast "
-                                       f"({dist.get_backend().upper()}) "
-                                       + ("inside every step" if scaling == "strong" else
-                                          "once, before the timed region")),
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                       "cuda_graph": bool(dev.get("graph"))},
+            "config": job_config(w, world),
+            "execution": {"dist_backend": dist.get_backend().upper() if world > 1 else None,
+                          "cuda_graph": bool(dev.get("graph"))},
             "e2e": {"value": round(e2e_value, 3), "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "moa_product_rows_host (C ABI) on page-locked host buffers"
-                    if world == 1 else "distributed.sharded_product_host"},
+                    if world == 1 else "distributed.sharded_product_host, max over ranks"},
             "gpu_launches": launches,
             **({"e2e_api": e2e_api} if e2e_api else {}),
-            "roofline": roofline(w, rows_range[1] - rows_range[0], kern_ms),
+            **({"e2e_pageable": e2e_pageable} if e2e_pageable else {}),
+            "roofline": roofline(w, rows_range[1] - rows_range[0], kern_ms,
+                                 dev["clocks"].get("sm_mhz")),
             "kernel_ms": round(kern_ms, 4),
             "clocks": dev["clocks"]}
 
-    if world == 1 and not args.no_inner and w.key == "c2":
+    inputs = {}
+    if not args.no_inner and w.key == "c2":
+        default_legs = ("c1", "c3", "c4", "c5") if world == 1 else ("c4", "c5")
         inner = {}
-        for key in [k for k in ("c1", "c3", "c4", "c5") if args.legs is None or k in args.legs]:
-            wi = WORKLOADS[key]
-            ai, bi = wi.generate()
-            mi = wi.mkn[0]
-            st = 20 if key in ("c1", "c3") else 3
-            d = measure_device(wi, (0, mi), ai, bi, st, 3, device, 1, 0)
-            amt = unit_amount(wi, mi)
-            inner[key] = {"metric": METRIC[key][0], "unit": METRIC[key][1],
-                          "value": round(to_unit(wi, amt, d["step_ms_total"] / st * 1e-3), 2),
-                          "kernel_ms": round(d["kernel_ms_mean"], 4),
-                          "roofline": roofline(wi, mi, d["kernel_ms_mean"]),
-                          "clocks": d["clocks"]}
-            # the same product end to end through moa.inner on pinned host
-            # arrays (H2D of A and B, the product, D2H of C inside the clock)
-            ap, bp = pinned_copy(ai), pinned_copy(bi)
-            e2e_st = 20 if key == "c1" else 3
-            el_i = measure_e2e(wi, (0, mi), ap, bp, e2e_st, 3, device, 1, 0)
-            isz_i = np.dtype(wi.dtype).itemsize
-            ki, ni = wi.mkn[1], wi.mkn[2]
-            el_c = measure_e2e_cabi(wi, ap, bp, e2e_st, 3, device)
-            inner[key]["e2e"] = {"value": round(to_unit(wi, amt * e2e_st, el_c), 2),
-                                 "unit": METRIC[key][1], "ms_per_step": round(el_c / e2e_st * 1e3, 3),
-                                 "h2d_bytes_per_step": (mi * ki + ki * ni) * isz_i,
-                                 "d2h_bytes_per_step": mi * ni * isz_i,
-                                 "path": "moa_product_rows_host (C ABI) on page-locked host "
-                                         "buffers (streamed row blocks)"}
-            inner[key]["e2e_api"] = {"value": round(to_unit(wi, amt * e2e_st, el_i), 2),
-                                     "unit": METRIC[key][1],
-                                     "ms_per_step": round(el_i / e2e_st * 1e3, 3),
-                                     "path": "moa.inner on pinned host MoaArrays (streamed row blocks)"}
-            del ap, bp
-            if rank == 0 and not args.no_cpu:
-                # the reference's own loop on a small row sample (~1-3 s of CPU)
-                rows_i = {"c1": mi, "c3": 1024, "c4": 32, "c5": 32}[key]
-                t_i, kind_i, cores_i, sample_i, rows_i = cpu_reference_time(
-                    wi, ai, bi, budget_s=1.5, rows=rows_i, min_reps=1)
-                inner[key]["cpu_baseline"] = {
-                    "value": round(to_unit(wi, unit_amount(wi, rows_i), t_i), 4),
-                    "unit": METRIC[key][1], "cores": cores_i, "kind": kind_i, "sample": sample_i}
-            del ai, bi
+        for key in [x for x in default_legs if args.legs is None or x in args.legs]:
+            inner[key], inputs[key] = inner_leg(key, device, world, rank)
+            if rank != 0 or args.no_cpu:
+                inputs.pop(key)
         line["inner"] = inner
 
-    if world > 1 and not args.no_inner and w.key == "c2":
-        # BASELINE configs 4-5 at N GPUs: result rows sharded over the ranks, B
-        # broadcast from rank 0 inside every step (strong scaling, max over ranks)
-        from paper_0907_0792_b200.distributed import row_block
-        inner = {}
-        for key in ("c4", "c5"):
-            wi = WORKLOADS[key]
-            ai, bi = wi.generate()
-            mi = wi.mkn[0]
-            rr = row_block(mi, world, rank)
-            st = 3
-            d = measure_device(wi, rr, ai, bi, st, 3, device, world, rank)
-            t = torch.tensor([d["step_ms_total"], d["kernel_ms_mean"]], dtype=torch.float64,
-                             device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            amt = unit_amount(wi, mi)
-            inner[key] = {"metric": METRIC[key][0], "unit": METRIC[key][1], "scaling": "strong",
-                          "value": round(to_unit(wi, amt, t[0].item() / st * 1e-3), 2),
-                          "rows_per_rank": rr[1] - rr[0],
-                          "kernel_ms": round(t[1].item(), 4),
-                          "roofline": roofline(wi, rr[1] - rr[0], t[1].item()),
-                          "clocks": d["clocks"]}
-            del ai, bi
-        line["inner"] = inner
-
-    if world == 1 and rank == 0 and not args.no_cpu:
-        t_unit, kind, cores, sample, rows = cpu_reference_time(w, a, b, rows=cpu_rows_for(w))
-        line["cpu_baseline"] = {"value": round(to_unit(w, unit_amount(w, rows), t_unit), 4),
-                                "unit": unit, "cores": cores, "kind": kind, "sample": sample}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if rank != 0:
+        return
+    # CPU legs last, on rank 0 alone, once every other rank has exited, so no
+    # GPU work or waiting rank competes for the host cores
+    if not args.no_cpu:
+        import oracle
+        cores = oracle.host_cores()
+        line["cpu_baseline"] = cpu_reference_time(w, a, b, cpu_rows_for(w, cores))
+        for key, (ai, bi) in inputs.items():
+            wi = WORKLOADS[key]
+            line["inner"][key]["cpu_baseline"] = cpu_reference_time(wi, ai, bi,
+                                                                    cpu_rows_for(wi, cores))
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

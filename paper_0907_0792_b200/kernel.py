@@ -32,10 +32,16 @@ from .ops import MUL_ADD, OpPair
 
 MAX_INDEX = 2**63 - 1
 
-BACKENDS = ("cuda",)
-DEFAULT_BACKEND = "cuda"
-# names accepted for the native backend; "compiled" keeps reference call sites working
-_BACKEND_ALIASES = {None: "cuda", "auto": "cuda", "cuda": "cuda", "compiled": "cuda"}
+# The CUDA library is this build's compiled backend, so it answers to the
+# reference's name (_backend.py:12, BACKENDS ``("compiled", "python")``);
+# "cuda" is accepted as an alias.  The reference's "python" backend is the
+# pure-Python loop (_purekernel.py); this build has no CPU path, so asking for
+# it raises ValueError, as the reference does for an unavailable backend
+# (_backend.py:23-24).
+BACKENDS = ("compiled",)
+DEFAULT_BACKEND = "compiled"
+_BACKEND_ALIASES = {None: "compiled", "auto": "compiled", "compiled": "compiled",
+                    "cuda": "compiled"}
 
 
 class ProductMode(enum.Enum):
@@ -111,6 +117,9 @@ def resolve_backend(backend: str | None, ops: OpPair) -> str:
     ValueError — the same error the reference gives when the compiled backend
     is requested explicitly.
     """
+    if backend == "python":
+        raise ValueError("python backend requested but this build has no CPU path "
+                         "(the products run on the CUDA backend only)")
     if backend not in _BACKEND_ALIASES:
         raise ValueError(f"unknown backend {backend!r}; choose from {BACKENDS}")
     if ops.codes() is None:

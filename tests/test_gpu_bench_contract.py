@@ -36,9 +36,11 @@ def test_default_line_contract():
     assert "workload" in d["config"]
     e2e = d["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert d["e2e_pageable"]["value"] > 0 and d["e2e_pageable"]["first_call_ms"] > 0
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert "theoretical" in r
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0
     assert d["clocks"]["sm_mhz"] is not None
@@ -48,6 +50,10 @@ def test_reference_arm_line():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "0")
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] >= 1
+    ours = _run("--steps", "3", "--warmup", "3", "--no-inner", "--no-cpu")
+    assert d["config"] == ours["config"]   # the driver's same_config check
+    for key in ("metric", "unit", "higher_is_better", "scaling", "dtype"):
+        assert d[key] == ours[key]
 
 
 def test_multi_rank_line_over_gloo():
@@ -74,3 +80,4 @@ def test_multi_rank_line_over_gloo():
     assert set(d["inner"]) == {"c4", "c5"}
     for leg in d["inner"].values():
         assert leg["scaling"] == "strong" and leg["rows_per_rank"] == 8192 and leg["value"] > 0
+        assert leg["e2e"]["value"] > 0 and leg["e2e"]["d2h_bytes_per_step"] > 0

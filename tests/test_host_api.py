@@ -244,16 +244,17 @@ def test_check_plan_detects_mismatch():
 
 
 def test_backend_names_and_custom_callables():
-    assert resolve_backend(None, moa.MUL_ADD) == "cuda"
-    assert resolve_backend("auto", moa.MUL_ADD) == "cuda"
-    assert resolve_backend("compiled", moa.MUL_ADD) == "cuda"
+    assert resolve_backend(None, moa.MUL_ADD) == "compiled"
+    assert resolve_backend("auto", moa.MUL_ADD) == "compiled"
+    assert resolve_backend("compiled", moa.MUL_ADD) == "compiled"
+    assert resolve_backend("cuda", moa.MUL_ADD) == "compiled"
     with pytest.raises(ValueError):
         resolve_backend("rust", moa.MUL_ADD)
     with pytest.raises(ValueError):
         resolve_backend("python", moa.MUL_ADD)  # no CPU path in this build
     with pytest.raises(ValueError):
         resolve_backend(None, OpPair(lambda x, y: x * y, lambda x, y: x + y, 0.0))
-    assert moa.active_backend() == "cuda"
+    assert moa.active_backend() == "compiled"  # the reference's name (_backend.py:12)
 
 
 # ---- partitions (reference tests/test_parallel.py:18-33) ----------------------
