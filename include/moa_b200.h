@@ -88,8 +88,16 @@ extern "C" {
  *
  * starting from the reduce identity (default) or from res (ACCUMULATE).
  * Bit-exact with the reference for every (combine, reduce) pair except
- * (multiply, add) without MOA_FLAG_EXACT, which runs on the FP64 tensor cores
- * with fused multiply-adds and is accurate to K*2^-52*max|A|*max|B|.
+ * (multiply, add) float64 with rowsinred >= 8 and without MOA_FLAG_EXACT,
+ * which runs on the FP64 tensor cores with fused multiply-adds and is
+ * accurate to K*2^-52*max|A|*max|B| over the finite operands, with the
+ * reference's NaN positions and infinities (signs included).  The one
+ * exception to the latter is overflow near DBL_MAX: where the reference's
+ * separately rounded product overflows to +-inf but the fused sum stays in
+ * range (or the reverse), the two differ — MOA_FLAG_EXACT reproduces the
+ * reference there too.  Below rowsinred = 8 (multiply, add) takes the exact
+ * fold (the product is bound by writing res either way), so small products —
+ * the reference's own random-case tests — return the reference's bits.
  * float32 operands follow the reference's upcast (arrays.py:77-78): the result
  * equals the reference's float64 result rounded to float32.
  */

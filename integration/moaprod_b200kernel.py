@@ -13,6 +13,20 @@ caller's rows of res, so concurrent callers never overwrite each other's
 rows.  Nothing but ctypes and numpy is imported; no torch in the reference's
 process.
 
+Rounding.  By default every call carries MOA_FLAG_EXACT too, so (multiply,
+add) folds with the reference's separate multiply and add in l order and the
+module is bit-identical to the compiled loop and the pure-Python backend for
+every op pair (the reference's tests/test_kernel.py::test_bitwise_equal_backends
+holds with it registered).  $MOA_B200_TENSOR_CORES=1 drops the flag: (multiply,
+add) with rowsinred >= 8 then runs on the FP64 tensor cores (DMMA, fused
+multiply-adds), accurate to K*2^-52*max|A|*max|B| instead of bit-identical.
+
+``product_rows_overwrite`` is the same call for a runner that does NOT prefill
+res with the identity (kernel.py:149): each row of the set is written from the
+identity in registers (bit-identical to prefill + accumulate), so res only
+travels device -> host and the 8-byte-per-element prefill pass disappears.
+INTEGRATION.md shows the two-line _Runner branch that uses it.
+
 The reference's execute_parallel calls this from W threads, worker k with
 rows k, k+W, ... (parallel.py:37-43); worker k runs on GPU DEVICES[k mod
 len(DEVICES)], so the reference's own fork-join spreads its row sets over the
@@ -44,14 +58,16 @@ _lib.moa_last_error.restype = ctypes.c_char_p
 _lib.moa_device_count.restype = ctypes.c_int
 MOA_DTYPE_F64 = 0
 MOA_FLAG_ACCUMULATE = 1
+MOA_FLAG_EXACT = 2
+# reference rounding unless the caller opts into the tensor-core route
+ROUND_FLAGS = 0 if os.environ.get("MOA_B200_TENSOR_CORES") == "1" else MOA_FLAG_EXACT
 DEVICES = ([int(d) for d in os.environ["MOA_B200_DEVICES"].split(",") if d.strip()]
            if os.environ.get("MOA_B200_DEVICES") else
            list(range(max(1, _lib.moa_device_count()))))
 
 
-def product_rows(res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restride,
-                 combine_code, reduce_code, start, step):
-    """Drop-in for _ckernel.product_rows (same arguments, float64 buffers)."""
+def _call(flags, res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restride,
+          combine_code, reduce_code, start, step):
     res = np.asarray(res)
     if res.dtype != np.float64 or not res.flags.c_contiguous or not res.flags.writeable:
         raise TypeError("res must be a writeable contiguous float64 buffer")
@@ -60,6 +76,22 @@ def product_rows(res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restri
     rc = _lib.moa_product_rows_host(MOA_DTYPE_F64, res.ctypes.data, a.ctypes.data, b.ctypes.data,
                                     noproc, rowsinred, elsinop, lstride, rstride, restride,
                                     combine_code, reduce_code, start, step,
-                                    MOA_FLAG_ACCUMULATE, DEVICES[start % len(DEVICES)])
+                                    flags | ROUND_FLAGS, DEVICES[start % len(DEVICES)])
     if rc != 0:
         raise RuntimeError(_lib.moa_last_error().decode())
+
+
+def product_rows(res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restride,
+                 combine_code, reduce_code, start, step):
+    """Drop-in for _ckernel.product_rows (same arguments, float64 buffers):
+    folds rows start::step INTO res."""
+    _call(MOA_FLAG_ACCUMULATE, res, a, b, noproc, rowsinred, elsinop, lstride, rstride,
+          restride, combine_code, reduce_code, start, step)
+
+
+def product_rows_overwrite(res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restride,
+                           combine_code, reduce_code, start, step):
+    """product_rows for an un-prefilled res: rows start::step are WRITTEN with
+    the fold from the reduce identity (what prefill + product_rows gives)."""
+    _call(0, res, a, b, noproc, rowsinred, elsinop, lstride, rstride, restride,
+          combine_code, reduce_code, start, step)

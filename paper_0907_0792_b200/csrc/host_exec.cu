@@ -17,14 +17,19 @@
 // arrives in k-slab-aligned chunks behind the first block's A rows and the
 // first block is computed chunk by chunk as they land (MOA_FLAG_ACCUMULATE),
 // wherever the fold replays exactly under chunked accumulation (everything but
-// float32 data folded in float64).  Copies overlap the kernels when the host
-// buffers are page-locked; pageable buffers are staged by the driver (same
-// results, lower bandwidth).
+// float32 data folded in float64).  Page-locked host buffers move with
+// asynchronous copies; pageable ones (plain numpy arrays) are staged through
+// page-locked slots by a small pool of host copy threads (host_runtime.cu), at
+// link speed instead of the driver's 11-22 GB/s pageable path.  Streams,
+// events and small device buffers come from a per-device pool of queue sets
+// (one per concurrent caller), large block buffers from a private device
+// memory pool, so a call costs a few API calls beyond its copies and kernels.
 #include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
 
+#include "host_runtime.h"
 #include "moa_common.cuh"
 #include "moa_kernels.h"
 #include "../../include/moa_b200.h"
@@ -91,89 +96,60 @@ std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K, int64
   return out;
 }
 
+// [0, K) in up to `chunks` ranges with inner boundaries on multiples of
+// `align`; a tail shorter than `align` joins the previous range, so every
+// chunk keeps the route (and fold) of the whole product (capi.cu route())
 std::vector<std::pair<int64_t, int64_t>> k_chunks(int64_t K, int chunks, int64_t align) {
   if (chunks <= 1 || K <= align) return {{0, K}};
   int64_t step = (K + chunks - 1) / chunks;
   step = (step + align - 1) / align * align;
   std::vector<std::pair<int64_t, int64_t>> out;
   for (int64_t k0 = 0; k0 < K; k0 += step) out.push_back({k0, k0 + step < K ? k0 + step : K});
+  if (out.size() > 1 && out.back().second - out.back().first < align) {
+    out[out.size() - 2].second = K;
+    out.pop_back();
+  }
   return out;
 }
 
-// Per-thread, per-device copy/compute queues, created on first use and kept
-// for the life of the thread (creating and destroying six streams per call
-// cost ~0.25 ms, which dominated small products).  One set per calling thread
-// keeps concurrent callers independent.
-struct Queues {
-  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
-  cudaStream_t s_aux[3] = {nullptr, nullptr, nullptr};  // extra copy-out queues
-};
-Queues* thread_queues(int device, cudaError_t& err) {
-  thread_local std::vector<std::pair<int, Queues>> cache;
-  for (auto& e : cache)
-    if (e.first == device) return &e.second;
-  Queues q;
-  cudaStream_t* all[6] = {&q.s_in, &q.s_comp, &q.s_out, &q.s_aux[0], &q.s_aux[1], &q.s_aux[2]};
-  for (cudaStream_t* s : all) {
-    err = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
-    if (err != cudaSuccess) return nullptr;
-  }
-  cache.emplace_back(device, q);
-  return &cache.back().second;
-}
-
-// one call's events and device buffers, released on every exit path
+// one call's resources: a pooled queue set (returned at the end) and the
+// block buffers drawn from the device's private pool
 struct Session {
   int prev_device = -1;
-  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
-  cudaStream_t s_aux[3] = {nullptr, nullptr, nullptr};
-  std::vector<cudaEvent_t> events;
-  std::vector<void*> buffers;
+  int device = -1;
+  moa::host::Queues* q = nullptr;
+  cudaMemPool_t pool = nullptr;
+  std::vector<void*> pooled;  // freed (stream-ordered) at the end
   cudaError_t err = cudaSuccess;
 
-  cudaEvent_t event() {
-    cudaEvent_t e = nullptr;
-    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    if (e) events.push_back(e);
-    return e;
-  }
-  void* alloc(size_t bytes) {
+  cudaEvent_t event() { return q->event(err); }
+  // small buffers come from the queue set's cache; large ones from the pool
+  void* alloc(int slot, size_t bytes, cudaStream_t st) {
+    if (err != cudaSuccess) return nullptr;
+    if (void* p = q->cached_buffer(slot, bytes, pool, st, err)) return p;
+    if (err != cudaSuccess) return nullptr;
     void* p = nullptr;
-    if (bytes == 0) bytes = 16;
-    if (err == cudaSuccess) err = cudaMallocAsync(&p, bytes, s_in);
-    if (p) buffers.push_back(p);
+    err = cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, st);
+    if (p) pooled.push_back(p);
     return p;
   }
   void check(cudaError_t e) {
     if (err == cudaSuccess && e != cudaSuccess) err = e;
   }
   ~Session() {
-    if (s_in) cudaStreamSynchronize(s_in);
-    if (s_comp) cudaStreamSynchronize(s_comp);
-    if (s_out) cudaStreamSynchronize(s_out);
-    for (cudaStream_t x : s_aux)
-      if (x) cudaStreamSynchronize(x);
-    for (void* p : buffers) cudaFreeAsync(p, s_in);
-    if (s_in) cudaStreamSynchronize(s_in);
-    for (cudaEvent_t e : events) cudaEventDestroy(e);
-    if (prev_device >= 0) cudaSetDevice(prev_device);
+    if (q) {
+      if (err != cudaSuccess || !pooled.empty()) {
+        // drain every queue before buffers or the queue set are reused
+        cudaStream_t all[6] = {q->s_in, q->s_comp, q->s_out, q->s_aux[0], q->s_aux[1], q->s_aux[2]};
+        for (cudaStream_t s : all) cudaStreamSynchronize(s);
+      }
+      for (void* p : pooled) cudaFreeAsync(p, q->s_in);
+      if (!pooled.empty()) cudaStreamSynchronize(q->s_in);
+      moa::host::checkin(q);
+    }
+    if (prev_device >= 0 && prev_device != device) cudaSetDevice(prev_device);
   }
 };
-
-// keep freed device memory in the device's default pool between calls
-void keep_pool_memory(int device) {
-  static std::mutex mu;
-  static std::vector<int> done;
-  std::lock_guard<std::mutex> lock(mu);
-  for (int d : done)
-    if (d == device) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t threshold = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
-  }
-  done.push_back(device);
-}
 
 int fail_cuda(cudaError_t e, const char* what) {
   moa::set_last_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -212,22 +188,23 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   const int64_t rows = (noproc - start + step - 1) / step;
 
   Session ss;
+  ss.device = device;
   int cur = 0;
   if (cudaGetDevice(&cur) == cudaSuccess) ss.prev_device = cur;
-  if (cudaError_t e = cudaSetDevice(device); e != cudaSuccess) {
-    (void)cudaGetLastError();  // not sticky: do not leave it for the next launch check
-    return fail_cuda(e, "cudaSetDevice");
+  if (cur != device) {
+    if (cudaError_t e = cudaSetDevice(device); e != cudaSuccess) {
+      (void)cudaGetLastError();  // not sticky: do not leave it for the next launch check
+      return fail_cuda(e, "cudaSetDevice");
+    }
   }
-  keep_pool_memory(device);
   {
     cudaError_t e = cudaSuccess;
-    Queues* q = thread_queues(device, e);
-    if (q == nullptr) return fail_cuda(e, "stream creation");
-    ss.s_in = q->s_in;
-    ss.s_comp = q->s_comp;
-    ss.s_out = q->s_out;
-    for (int i = 0; i < 3; i++) ss.s_aux[i] = q->s_aux[i];
+    ss.q = moa::host::checkout(device, e);
+    if (ss.q == nullptr) return fail_cuda(e, "stream creation");
+    ss.pool = moa::host::device_pool(device, e);
+    if (ss.pool == nullptr) return fail_cuda(e, "device memory pool");
   }
+  moa::host::Queues& q = *ss.q;
 
   // A rows of the set pack densely (lda = K) when the set's rows do not
   // overlap; otherwise the whole span of A goes over with its own strides
@@ -235,150 +212,215 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   const bool b_dense = K == 0 || rstride >= N;
   const char* a_rows = static_cast<const char*>(a) + (size_t)(start * lstride) * esz;
   char* c_rows = static_cast<char*>(res) + (size_t)(start * restride) * esz;
+  // page-locked host buffers move with asynchronous copies; pageable ones are
+  // staged through page-locked slots by the copy threads (host_runtime.cu)
+  const bool a_pin = K == 0 || moa::host::is_pinned(a);
+  const bool b_pin = K == 0 || moa::host::is_pinned(b);
+  const bool r_pin = moa::host::is_pinned(res);
+  const size_t a_pitch = (size_t)(lstride * step) * esz, c_pitch = (size_t)(restride * step) * esz;
 
   const bool wide = dtype == MOA_DTYPE_F32 &&
                     (reduce_code == moa::R_ADD || reduce_code == moa::R_MUL || combine_code == moa::C_MUL ||
                      combine_code == moa::C_DIV);
   std::vector<Block> blocks = (a_dense && b_dense)
                                   ? plan_blocks(rows, rows * N * (int64_t)esz, K, (K + N) * (int64_t)esz)
-                                                   : std::vector<Block>{{0, rows}};
+                                  : std::vector<Block>{{0, rows}};
   const bool chunked = blocks.size() > 1 && !wide && K >= 2;
   const auto chunks = chunked ? k_chunks(K, blocks.size() >= 5 ? 8 : (int)blocks.size(), 16)
                               : std::vector<std::pair<int64_t, int64_t>>{{0, K}};
 
-  // device buffers
   int64_t max_rows = 0;
   for (const Block& bl : blocks) max_rows = bl.r1 - bl.r0 > max_rows ? bl.r1 - bl.r0 : max_rows;
-  const int nslots = blocks.size() > 1 ? 2 : 1;
   const int64_t a_span = a_dense ? max_rows * K : ((rows - 1) * lstride * step + K);
   const int64_t b_span = b_dense ? K * N : ((K - 1) * rstride + N);
   const int64_t lda = a_dense ? K : lstride * step, ldb = b_dense ? N : rstride;
+
+  // A of the set (dense rows, or the whole strided span), B, onto the device
+  auto copy_a = [&](char* dst, int64_t r0, int64_t nr, int64_t k0, int64_t k1, cudaStream_t st) {
+    if (a_dense)
+      ss.check(moa::host::h2d(device, dst + (size_t)k0 * esz, (size_t)K * esz,
+                              a_rows + (size_t)r0 * a_pitch + (size_t)k0 * esz, a_pitch,
+                              (size_t)(k1 - k0) * esz, (size_t)nr, a_pin, st));
+    else
+      ss.check(moa::host::h2d(device, dst, (size_t)a_span * esz, a_rows, (size_t)a_span * esz,
+                              (size_t)a_span * esz, 1, a_pin, st));
+  };
+  auto copy_b = [&](char* dst, int64_t k0, int64_t k1, cudaStream_t st) {
+    if (b_dense)
+      ss.check(moa::host::h2d(device, dst + (size_t)(k0 * N) * esz, (size_t)N * esz,
+                              static_cast<const char*>(b) + (size_t)(k0 * rstride) * esz,
+                              (size_t)rstride * esz, (size_t)N * esz, (size_t)(k1 - k0), b_pin, st));
+    else
+      ss.check(moa::host::h2d(device, dst, (size_t)b_span * esz, b, (size_t)b_span * esz,
+                              (size_t)b_span * esz, 1, b_pin, st));
+  };
+
+  // ---- one block: everything in order on one queue, no events
+  if (blocks.size() == 1) {
+    cudaStream_t st = q.s_comp;
+    char* a_dev = static_cast<char*>(ss.alloc(0, (size_t)(K > 0 ? a_span : 0) * esz, st));
+    char* b_dev = static_cast<char*>(ss.alloc(1, (size_t)(K > 0 ? b_span : 0) * esz, st));
+    char* c_dev = static_cast<char*>(ss.alloc(2, (size_t)(rows * N) * esz, st));
+    if (ss.err != cudaSuccess) return fail_cuda(ss.err, "device buffers");
+    if (K > 0) {
+      copy_a(a_dev, 0, rows, 0, K, st);
+      copy_b(b_dev, 0, K, st);
+    }
+    if (acc)
+      ss.check(moa::host::h2d(device, c_dev, (size_t)N * esz, c_rows, c_pitch, (size_t)N * esz,
+                              (size_t)rows, r_pin, st));
+    if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product (copy in)");
+    const int rc = moa_product_rows(dtype, c_dev, K > 0 ? a_dev : nullptr, K > 0 ? b_dev : nullptr,
+                                    rows, K, N, K > 0 ? lda : 0, K > 0 ? ldb : N, N, combine_code,
+                                    reduce_code, 0, 1, flags, st);
+    if (rc != 0) {
+      ss.err = cudaErrorUnknown;  // drain before the queues are reused; message already set
+      return rc;
+    }
+    const size_t out_bytes = (size_t)(rows * N) * esz;
+    if (r_pin && rows >= 4 && out_bytes >= (64ull << 20)) {
+      // a large result leaves over four copy queues, which draw a little
+      // more of the host link than one (tools/e2e_probe.py: 54.8 -> 56.9 GB/s)
+      cudaEvent_t done = ss.event();
+      ss.check(cudaEventRecord(done, st));
+      const int64_t per = (rows + 3) / 4;
+      cudaStream_t qs[4] = {st, q.s_aux[0], q.s_aux[1], q.s_aux[2]};
+      for (int i = 0; i < 4; i++) {
+        const int64_t r0 = i * per, r1 = (i + 1) * per < rows ? (i + 1) * per : rows;
+        if (r0 >= r1) break;
+        if (i > 0) ss.check(cudaStreamWaitEvent(qs[i], done, 0));
+        ss.check(moa::host::d2h(device, c_rows + (size_t)r0 * c_pitch, c_pitch,
+                                c_dev + (size_t)(r0 * N) * esz, (size_t)N * esz, (size_t)N * esz,
+                                (size_t)(r1 - r0), true, qs[i]));
+      }
+      for (cudaStream_t x : qs) ss.check(cudaStreamSynchronize(x));
+    } else {
+      ss.check(moa::host::d2h(device, c_rows, c_pitch, c_dev, (size_t)N * esz, (size_t)N * esz,
+                              (size_t)rows, r_pin, st));
+      ss.check(cudaStreamSynchronize(st));
+    }
+    if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product");
+    return 0;
+  }
+
+  // ---- streamed row blocks (results of >= 1 GiB)
   char* a_buf[2] = {nullptr, nullptr};
   char* c_buf[2] = {nullptr, nullptr};
-  for (int s = 0; s < nslots; s++) {
-    a_buf[s] = static_cast<char*>(ss.alloc((size_t)(K > 0 ? a_span : 0) * esz));
-    c_buf[s] = static_cast<char*>(ss.alloc((size_t)(max_rows * N) * esz));
+  for (int s = 0; s < 2; s++) {
+    a_buf[s] = static_cast<char*>(ss.alloc(-1, (size_t)(K > 0 ? a_span : 0) * esz, q.s_in));
+    c_buf[s] = static_cast<char*>(ss.alloc(-1, (size_t)(max_rows * N) * esz, q.s_in));
   }
-  char* b_buf = static_cast<char*>(ss.alloc((size_t)(K > 0 ? b_span : 0) * esz));
+  char* b_buf = static_cast<char*>(ss.alloc(-1, (size_t)(K > 0 ? b_span : 0) * esz, q.s_in));
   cudaEvent_t allocated = ss.event();
-  ss.check(cudaEventRecord(allocated, ss.s_in));
-  ss.check(cudaStreamWaitEvent(ss.s_comp, allocated, 0));
-  ss.check(cudaStreamWaitEvent(ss.s_out, allocated, 0));
+  ss.check(cudaEventRecord(allocated, q.s_in));
+  ss.check(cudaStreamWaitEvent(q.s_comp, allocated, 0));
+  ss.check(cudaStreamWaitEvent(q.s_out, allocated, 0));
   if (ss.err != cudaSuccess) return fail_cuda(ss.err, "device buffers");
 
   std::vector<cudaEvent_t> b_ready;
   cudaEvent_t a_free[2] = {nullptr, nullptr}, c_free[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> done(blocks.size(), nullptr);
 
-  // result rows of block i back into res; a large block is split over four
-  // copy queues, which draw a little more of the host link than one
-  // (tools/e2e_probe.py: 54.8 -> 56.9 GB/s)
+  // result rows of block i back into res: page-locked res over four copy
+  // queues (asynchronous); pageable res staged by the copy threads (returns
+  // when the rows are in res, while the next block computes)
   auto copy_out = [&](size_t i) {
     const Block& bl = blocks[i];
-    const int slot = (int)(i % nslots);
+    const int slot = (int)(i % 2);
     const int64_t nr = bl.r1 - bl.r0;
-    const int parts = (nr >= 4 && nr * N * (int64_t)esz >= (64ll << 20)) ? 4 : 1;
-    const int64_t per = (nr + parts - 1) / parts;
-    std::vector<cudaEvent_t> joined;
-    for (int q = 0; q < parts && ss.err == cudaSuccess; q++) {
-      const int64_t q0 = q * per, q1 = (q + 1) * per < nr ? (q + 1) * per : nr;
-      if (q0 >= q1) break;
-      cudaStream_t st = q > 0 ? ss.s_aux[q - 1] : ss.s_out;
-      ss.check(cudaStreamWaitEvent(st, done[i], 0));
-      ss.check(cudaMemcpy2DAsync(c_rows + (size_t)((bl.r0 + q0) * restride * step) * esz,
-                                 (size_t)(restride * step) * esz,
-                                 c_buf[slot] + (size_t)(q0 * N) * esz, (size_t)N * esz,
-                                 (size_t)N * esz, (size_t)(q1 - q0), cudaMemcpyDeviceToHost, st));
-      if (q > 0) {
-        joined.push_back(ss.event());
-        ss.check(cudaEventRecord(joined.back(), st));
+    char* host_rows = c_rows + (size_t)bl.r0 * c_pitch;
+    if (!r_pin) {
+      ss.check(cudaStreamWaitEvent(q.s_out, done[i], 0));
+      ss.check(moa::host::d2h(device, host_rows, c_pitch, c_buf[slot], (size_t)N * esz,
+                              (size_t)N * esz, (size_t)nr, false, q.s_out));
+    } else {
+      const int parts = (nr >= 4 && nr * N * (int64_t)esz >= (64ll << 20)) ? 4 : 1;
+      const int64_t per = (nr + parts - 1) / parts;
+      std::vector<cudaEvent_t> joined;
+      for (int p = 0; p < parts && ss.err == cudaSuccess; p++) {
+        const int64_t q0 = p * per, q1 = (p + 1) * per < nr ? (p + 1) * per : nr;
+        if (q0 >= q1) break;
+        cudaStream_t st = p > 0 ? q.s_aux[p - 1] : q.s_out;
+        ss.check(cudaStreamWaitEvent(st, done[i], 0));
+        ss.check(moa::host::d2h(device, host_rows + (size_t)q0 * c_pitch, c_pitch,
+                                c_buf[slot] + (size_t)(q0 * N) * esz, (size_t)N * esz,
+                                (size_t)N * esz, (size_t)(q1 - q0), true, st));
+        if (p > 0) {
+          joined.push_back(ss.event());
+          ss.check(cudaEventRecord(joined.back(), st));
+        }
       }
+      for (cudaEvent_t e : joined) ss.check(cudaStreamWaitEvent(q.s_out, e, 0));
     }
-    for (cudaEvent_t e : joined) ss.check(cudaStreamWaitEvent(ss.s_out, e, 0));
     c_free[slot] = ss.event();
-    ss.check(cudaEventRecord(c_free[slot], ss.s_out));
+    ss.check(cudaEventRecord(c_free[slot], q.s_out));
   };
 
   for (size_t i = 0; i < blocks.size() && ss.err == cudaSuccess; i++) {
     const Block& bl = blocks[i];
-    const int slot = (int)(i % nslots);
+    const int slot = (int)(i % 2);
     const int64_t nr = bl.r1 - bl.r0;
     // --- in: this block's A rows (and res rows when accumulating), B behind block 0.
     // The first block, computed per k-chunk, takes its A rows in the same
     // k-chunks (2-D copies of a column range), each just ahead of the matching
     // B chunk, so the first kernel waits for one chunk of each, not all of A0.
     const bool a_by_chunk = i == 0 && chunks.size() > 1 && a_dense;
-    if (a_free[slot]) ss.check(cudaStreamWaitEvent(ss.s_in, a_free[slot], 0));
-    if (K > 0 && !a_by_chunk) {
-      if (a_dense)
-        ss.check(cudaMemcpy2DAsync(a_buf[slot], (size_t)K * esz,
-                                   a_rows + (size_t)(bl.r0 * lstride * step) * esz,
-                                   (size_t)(lstride * step) * esz, (size_t)K * esz, (size_t)nr,
-                                   cudaMemcpyHostToDevice, ss.s_in));
-      else
-        ss.check(cudaMemcpyAsync(a_buf[slot], a_rows, (size_t)a_span * esz, cudaMemcpyHostToDevice,
-                                 ss.s_in));
-    }
+    if (a_free[slot]) ss.check(cudaStreamWaitEvent(q.s_in, a_free[slot], 0));
+    if (K > 0 && !a_by_chunk) copy_a(a_buf[slot], bl.r0, nr, 0, K, q.s_in);
     if (acc) {
-      if (c_free[slot]) ss.check(cudaStreamWaitEvent(ss.s_in, c_free[slot], 0));
-      ss.check(cudaMemcpy2DAsync(c_buf[slot], (size_t)N * esz,
-                                 c_rows + (size_t)(bl.r0 * restride * step) * esz,
-                                 (size_t)(restride * step) * esz, (size_t)N * esz, (size_t)nr,
-                                 cudaMemcpyHostToDevice, ss.s_in));
+      if (c_free[slot]) ss.check(cudaStreamWaitEvent(q.s_in, c_free[slot], 0));
+      ss.check(moa::host::h2d(device, c_buf[slot], (size_t)N * esz, c_rows + (size_t)bl.r0 * c_pitch,
+                              c_pitch, (size_t)N * esz, (size_t)nr, r_pin, q.s_in));
     }
     cudaEvent_t a_ready = ss.event();
-    ss.check(cudaEventRecord(a_ready, ss.s_in));
+    ss.check(cudaEventRecord(a_ready, q.s_in));
     if (i == 0 && K > 0) {
       for (const auto& ch : chunks) {
-        if (a_by_chunk)
-          ss.check(cudaMemcpy2DAsync(a_buf[slot] + (size_t)ch.first * esz, (size_t)K * esz,
-                                     a_rows + (size_t)(bl.r0 * lstride * step + ch.first) * esz,
-                                     (size_t)(lstride * step) * esz,
-                                     (size_t)(ch.second - ch.first) * esz, (size_t)nr,
-                                     cudaMemcpyHostToDevice, ss.s_in));
-        if (b_dense)
-          ss.check(cudaMemcpy2DAsync(b_buf + (size_t)(ch.first * N) * esz, (size_t)N * esz,
-                                     static_cast<const char*>(b) + (size_t)(ch.first * rstride) * esz,
-                                     (size_t)rstride * esz, (size_t)N * esz,
-                                     (size_t)(ch.second - ch.first), cudaMemcpyHostToDevice, ss.s_in));
-        else
-          ss.check(cudaMemcpyAsync(b_buf, b, (size_t)b_span * esz, cudaMemcpyHostToDevice, ss.s_in));
+        if (a_by_chunk) copy_a(a_buf[slot], bl.r0, nr, ch.first, ch.second, q.s_in);
+        copy_b(b_buf, b_dense ? ch.first : 0, b_dense ? ch.second : K, q.s_in);
         b_ready.push_back(ss.event());
-        ss.check(cudaEventRecord(b_ready.back(), ss.s_in));
+        ss.check(cudaEventRecord(b_ready.back(), q.s_in));
       }
     }
     // --- compute
-    ss.check(cudaStreamWaitEvent(ss.s_comp, a_ready, 0));
-    if (!acc && c_free[slot]) ss.check(cudaStreamWaitEvent(ss.s_comp, c_free[slot], 0));
+    ss.check(cudaStreamWaitEvent(q.s_comp, a_ready, 0));
+    if (!acc && c_free[slot]) ss.check(cudaStreamWaitEvent(q.s_comp, c_free[slot], 0));
     if (ss.err != cudaSuccess) break;
     const bool per_chunk = i == 0 && chunks.size() > 1;
     if (K > 0) {
       for (size_t j = 0; j < (per_chunk ? chunks.size() : 1); j++) {
         // blocks after the first read all of B: wait for its last chunk
-        ss.check(cudaStreamWaitEvent(ss.s_comp, per_chunk ? b_ready[j] : b_ready.back(), 0));
+        ss.check(cudaStreamWaitEvent(q.s_comp, per_chunk ? b_ready[j] : b_ready.back(), 0));
         const int64_t k0 = per_chunk ? chunks[j].first : 0, k1 = per_chunk ? chunks[j].second : K;
         const uint32_t f = (flags & ~MOA_FLAG_ACCUMULATE) |
                            ((acc || (per_chunk && j > 0)) ? MOA_FLAG_ACCUMULATE : 0u);
         const int rc = moa_product_rows(dtype, c_buf[slot], a_buf[slot] + (size_t)k0 * esz,
                                         b_buf + (size_t)(k0 * ldb) * esz, nr, k1 - k0, N, lda,
-                                        ldb, N, combine_code, reduce_code, 0, 1, f, ss.s_comp);
-        if (rc != 0) return rc;  // message already set; the session drains and frees
+                                        ldb, N, combine_code, reduce_code, 0, 1, f, q.s_comp);
+        if (rc != 0) {
+          ss.err = cudaErrorUnknown;  // drain; message already set
+          return rc;
+        }
       }
     } else {
       const int rc = moa_product_rows(dtype, c_buf[slot], nullptr, nullptr, nr, 0, N, 0, N, N,
-                                      combine_code, reduce_code, 0, 1, flags, ss.s_comp);
-      if (rc != 0) return rc;
+                                      combine_code, reduce_code, 0, 1, flags, q.s_comp);
+      if (rc != 0) {
+        ss.err = cudaErrorUnknown;
+        return rc;
+      }
     }
     done[i] = ss.event();
-    ss.check(cudaEventRecord(done[i], ss.s_comp));
+    ss.check(cudaEventRecord(done[i], q.s_comp));
     a_free[slot] = done[i];
     // --- out: the previous block's rows (issued after this block's kernel,
-    // so a blocking copy from pageable memory never stalls the GPU)
+    // so a staged copy into pageable memory runs while the GPU computes)
     if (i > 0) copy_out(i - 1);
   }
   if (ss.err == cudaSuccess) copy_out(blocks.size() - 1);
-  if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(ss.s_out));
-  if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(ss.s_comp));
+  if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_out));
+  if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_comp));
+  if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_in));
   if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product");
   return 0;
 }

@@ -49,13 +49,19 @@ def block_plan(plan: KernelPlan, r0: int, r1: int) -> KernelPlan:
 
 def broadcast_operand(b, plan: KernelPlan, *, src: int = 0, group=None, device=None,
                       dtype=None):
-    """B (rowsinred x elsinop, flat) on every rank; ``b`` is only read on ``src``."""
+    """B (rowsinred x elsinop, flat) on every rank; ``b`` is only read on ``src``.
+
+    Every rank must post the same byte count, so ``src`` sends B in ``dtype``
+    (the dtype the other ranks allocate), casting if ``b`` differs, and checks
+    B's length against the plan before the collective."""
     torch, dist = _torch(), _dist()
     n = plan.rowsinred * plan.elsinop
     if dist.get_rank(group) == src:
         buf = b.reshape(-1)
-        if device is not None:
-            buf = buf.to(device)
+        if buf.numel() != n:
+            raise ValueError(f"B holds {buf.numel()} elements; the plan needs {n}")
+        buf = buf.to(device=device if device is not None else buf.device,
+                     dtype=dtype if dtype is not None else buf.dtype)
         buf = buf.contiguous()
     else:
         buf = torch.empty(n, dtype=dtype if dtype is not None else b.dtype,
@@ -76,7 +82,12 @@ def k_chunks(K: int, chunks: int, align: int = 16) -> list[tuple[int, int]]:
         return [(0, K)]
     step = -(-K // chunks)
     step = -(-step // align) * align
-    return [(k0, min(K, k0 + step)) for k0 in range(0, K, step)]
+    out = [(k0, min(K, k0 + step)) for k0 in range(0, K, step)]
+    if len(out) > 1 and out[-1][1] - out[-1][0] < align:
+        # a short tail joins the previous chunk: every chunk keeps >= align
+        # k-steps, so its kernel route is the whole product's (capi.cu route())
+        out[-2:] = [(out[-2][0], K)]
+    return out
 
 
 # (combine, reduce) codes whose fold replays exactly when split into k-chunks
@@ -140,7 +151,10 @@ def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, grou
     # pipelined: async, in-order broadcasts of B's k-chunks; compute chases them
     n, k = plan.elsinop, plan.rowsinred
     if rank == src:
-        b_all = b.reshape(-1).to(a_block.device).contiguous()
+        # B in A's dtype, so every rank's chunk broadcasts post equal byte counts
+        b_all = b.reshape(-1).to(device=a_block.device, dtype=a_block.dtype).contiguous()
+        if b_all.numel() != k * n:
+            raise ValueError(f"B holds {b_all.numel()} elements; the plan needs {k * n}")
     else:
         b_all = torch.empty(k * n, dtype=a_block.dtype, device=a_block.device)
     chunks = k_chunks(k, bcast_chunks, align)

@@ -52,6 +52,9 @@ def test_header_constants_match_python_codes():
 def test_kernel_routing():
     pk = _native.plan_kernel
     assert pk(0, 16384, 16384, 16384, 2, 0) == "dmma"
+    assert pk(0, 16384, 8, 16384, 2, 0) == "dmma"
+    assert pk(0, 16384, 7, 16384, 2, 0) == "semiring_exact"  # write-bound: exact fold
+    assert pk(0, 4, 2, 4, 2, 0) == "semiring_exact"
     assert pk(0, 16384, 16384, 16384, 2, 0, _native.FLAG_EXACT) == "semiring_exact"
     assert pk(1, 16384, 16384, 16384, 0, 2) == "semiring_fast"
     # accumulate folds C's contents too (pre-scanned with A and B)

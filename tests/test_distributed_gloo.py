@@ -38,7 +38,7 @@ def _worker(rank, world, port, mode, q):
         from paper_0907_0792_b200.distributed import gather_rows, row_block, sharded_product
 
         rng = np.random.default_rng(5)
-        if mode == "inner":
+        if mode in ("inner", "inner_b_f32"):
             m, k, n = 37, 11, 9
             plan = moa.plan_inner((m, k), (k, n))
             ops = moa.op_pair("add", "min")
@@ -48,10 +48,15 @@ def _worker(rank, world, port, mode, q):
             ops = moa.op_pair("subtract", "max")
         a = rng.uniform(-1, 1, m * k)
         b = rng.uniform(-1, 1, k * n)
+        if mode == "inner_b_f32":
+            # B handed to rank 0 in another dtype than A: rank 0 must still
+            # post A's dtype to the broadcast (equal byte counts on every rank)
+            b = b.astype(np.float32).astype(np.float64)
         r0, r1 = row_block(m, world, rank)
         a_blk = torch.from_numpy(a[r0 * plan.lstride:r1 * plan.lstride].copy())
         # only rank 0 holds B; the others must receive it through the broadcast
-        b_arg = torch.from_numpy(b) if rank == 0 else None
+        b_arg = (torch.from_numpy(b.astype(np.float32)) if mode == "inner_b_f32"
+                 else torch.from_numpy(b)) if rank == 0 else None
         blk = sharded_product(plan, a_blk, b_arg, ops, row_kernel=_oracle_rows)
         assert blk.numel() == (r1 - r0) * n
         full = gather_rows(blk, plan)
@@ -67,7 +72,7 @@ def _worker(rank, world, port, mode, q):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("mode", ["inner", "outer"])
+@pytest.mark.parametrize("mode", ["inner", "outer", "inner_b_f32"])
 def test_sharded_product_gloo(world, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

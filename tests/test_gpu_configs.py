@@ -103,6 +103,55 @@ def test_tropical_config_c5_bit_exact():
     assert torch.equal(torch.isinf(out.data.view(m, n)), finite_pairs == 0)
 
 
+def _bits_equal_dev(got, want, msg):
+    """Bitwise equality of two CUDA float32 tensors, NaN payloads aside."""
+    import torch
+    gn, wn = torch.isnan(got), torch.isnan(want)
+    assert torch.equal(gn, wn), f"{msg}: NaN positions differ"
+    g = got.masked_fill(gn, 0).view(torch.int32)
+    w = want.masked_fill(wn, 0).view(torch.int32)
+    diff = int((g != w).sum().item())
+    assert diff == 0, f"{msg}: {diff} of {g.numel()} elements differ"
+
+
+@pytest.mark.parametrize("poison", ["none", "negatives", "nan_negzero"])
+def test_c5_whole_output_bitwise_against_exact_fold(poison):
+    """All 268M elements of the c5 product on the fast route, bit for bit
+    against the exact fold: the same inputs upcast to float64 through the
+    exact K2 route (bit-pinned to the reference's goldens and to the
+    reference's own c5 rows) and rounded once to float32 on the device — the
+    reference's result (arrays.py:77-78 upcasts, then float32 is the one
+    rounding).  ``none`` is BASELINE c5 (unsigned-order VIMNMX3 fold);
+    ``negatives`` forces the FMNMX3 fold (signed operands, no NaN or -0
+    result possible); ``nan_negzero`` forces the exact loop (a NaN and -0.0
+    in A) — every one of the device-chosen folds checked at full size."""
+    import torch
+    w, a, b, _, _ = _arrays("c5", device=False)
+    m, k, n = w.mkn
+    a = a.copy()
+    if poison == "negatives":
+        rng = np.random.default_rng(44)
+        idx = rng.choice(a.size, 1 << 16, replace=False)
+        a[idx] = -a[idx]
+        a[idx[:7]] = -np.inf
+    elif poison == "nan_negzero":
+        a[12345] = np.nan
+        a[(m - 1) * k + 17] = np.nan
+        a[777] = -0.0
+    A = MoaArray(w.shape_a, a, dtype=np.float32).to_device()
+    B = MoaArray(w.shape_b, b, dtype=np.float32).to_device()
+    fast = moa.inner(A, B, w.ops).data
+    A64 = MoaArray._wrap(w.shape_a, A.data.to(torch.float64))
+    B64 = MoaArray._wrap(w.shape_b, B.data.to(torch.float64))
+    assert moa.kernel._native.plan_kernel(0, m, k, n, 0, 2) == "semiring_exact"
+    ref = moa.inner(A64, B64, w.ops).data.to(torch.float32)
+    del A64, B64
+    _bits_equal_dev(fast, ref, f"c5 {poison}")
+    if poison == "none":  # and the reference's own rows, hashed
+        got = _rows(fast, PINS["c5"]["rows"], n)
+        assert hashlib.sha256(got.tobytes()).hexdigest() == PINS["c5"]["sha256_f32"]
+
+
 def test_c5_rows_sharded_any_gpu_count_bitwise():
     """Row blocks for 2/4/8 shards reproduce the one-shot result bit for bit."""
     import torch

@@ -209,3 +209,85 @@ def test_host_entry_bounded_blocks(monkeypatch, rng):
         got, ref = res.reshape(m, n), want.reshape(m, n)
         assert_bits_equal(got[1::2].ravel(), ref[1::2].ravel(), f"{ops} {dt.__name__} rows 1::2")
         assert np.all(got[0::2] == 5)
+
+
+def _pinned_like(x):
+    torch = _torch()
+    t = torch.empty(x.size, dtype=torch.from_numpy(x[:1]).dtype, pin_memory=True).numpy()
+    t[:] = x
+    return t
+
+
+@pytest.mark.parametrize("acc", [False, True])
+def test_pageable_staging_equals_page_locked(acc, rng):
+    """Pageable host buffers above the direct-copy size are staged through
+    page-locked slots by the executor's copy threads (host_runtime.cu): many
+    8 MiB chunks, strided row sets gathered and scattered by the threads,
+    accumulate mode reading res through the slots — the same bits as the
+    page-locked path."""
+    m, k, n = 1500, 700, 2300   # A 8 MiB, B 12.3 MiB, C 26 MiB: several chunks each
+    a, b = rng.random(m * k) * 2 - 1, rng.random(k * n) * 2 - 1
+    plan = plan_inner((m, k), (k, n))
+    for ops in (moa.MUL_ADD, op_pair("add", "min")):
+        for start, step in ((0, 1), (3, 5)):
+            res0 = rng.random(m * n) if acc else np.full(m * n, -1.5)
+            pinned = _pinned_like(res0)
+            launch_host(plan, pinned, _pinned_like(a), _pinned_like(b), ops, start=start,
+                        step=step, accumulate=acc)
+            pageable = res0.copy()
+            launch_host(plan, pageable, a, b, ops, start=start, step=step, accumulate=acc)
+            assert_bits_equal(pageable, pinned, f"{ops} {start}::{step} acc={acc}")
+            if step > 1:  # rows outside the set untouched
+                keep = np.setdiff1d(np.arange(m), np.arange(start, m, step))
+                assert_bits_equal(pageable.reshape(m, n)[keep].ravel(),
+                                  res0.reshape(m, n)[keep].ravel())
+
+
+def test_pageable_rows_wider_than_a_staging_slot(rng):
+    """Result rows longer than one 8 MiB staging slot move in row segments."""
+    m, n = 3, 1_300_000          # 10.4 MB per float64 row
+    x, y = rng.random(m) * 2 - 1, rng.random(n) * 2 - 1
+    res = np.empty(m * n)
+    launch_host(plan_outer((m,), (n,)), res, x, y, moa.MUL_ADD)
+    assert_bits_equal(res, (np.multiply.outer(x, y) + 0.0).ravel())
+    # and a K > 1 product whose B rows exceed a slot (pageable B, A, res)
+    k = 4
+    a, b = rng.random(m * k), rng.random(k * n)
+    res = np.empty(m * n)
+    launch_host(plan_inner((m, k), (k, n)), res, a, b, op_pair("add", "max"))
+    assert_bits_equal(res, oracle.product(a, b, m, k, n, 0, 3))
+
+
+def test_concurrent_pageable_callers_share_the_slots(rng):
+    """16 threads at once on pageable buffers (more slot demand than the
+    per-GPU slot budget): every caller still gets its exact result."""
+    from concurrent.futures import ThreadPoolExecutor
+    m, k, n = 600, 64, 1800
+    a, b = rng.random(m * k), rng.random(k * n)
+    plan = plan_inner((m, k), (k, n))
+    want = oracle.product(a, b, m, k, n, 0, 2)
+
+    def one(i):
+        res = np.full(m * n, np.nan)
+        launch_host(plan, res, a, b, op_pair("add", "min"))
+        return res
+    with ThreadPoolExecutor(16) as pool:
+        for got in pool.map(one, range(48)):
+            assert_bits_equal(got, want)
+
+
+def test_short_lived_threads_reuse_pooled_queues(rng):
+    """The reference's execute_parallel makes a new thread pool per call
+    (parallel.py:37-41); queue sets are pooled per device, not per thread, so
+    hundreds of short-lived calling threads neither leak streams nor fail."""
+    from concurrent.futures import ThreadPoolExecutor
+    m, k, n = 40, 16, 24
+    a, b = rng.random(m * k), rng.random(k * n)
+    plan = plan_inner((m, k), (k, n))
+    want = oracle.product(a, b, m, k, n, 2, 3)
+    for _ in range(60):
+        res = np.empty(m * n)
+        with ThreadPoolExecutor(4) as pool:
+            list(pool.map(lambda w: launch_host(plan, res, a, b, op_pair("multiply", "max"),
+                                                start=w, step=4), range(4)))
+        assert_bits_equal(res, want)

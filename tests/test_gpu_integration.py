@@ -3,7 +3,9 @@ the way the reference drives its compiled loop: ``_Runner`` prefills res with
 the reduce identity (kernel.py:149) and ``execute_parallel`` calls
 ``product_rows(res, a, b, ..., start=w, step=W)`` from W threads at once on
 one shared res (parallel.py:26-43).  Results must equal the reference's loop
-(oracle C port), bitwise except (multiply, add) on the FP64 tensor cores."""
+(oracle C port) bit for bit — (multiply, add) included, since the module
+sends MOA_FLAG_EXACT by default; with $MOA_B200_TENSOR_CORES=1 (multiply, add)
+runs on the FP64 tensor cores and is checked against K*2^-52*max|A|*max|B|."""
 
 from __future__ import annotations
 
@@ -44,7 +46,11 @@ def test_backend_module_binds_the_abi():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("workers", [1, 3, 8])
-def test_reference_style_runner_with_concurrent_threads(workers, rng):
+@pytest.mark.parametrize("tensor_cores", [False, True])
+def test_reference_style_runner_with_concurrent_threads(workers, tensor_cores, rng,
+                                                         monkeypatch):
+    if tensor_cores:
+        monkeypatch.setenv("MOA_B200_TENSOR_CORES", "1")
     mod = _module()
     m, k, n = 150, 37, 90
     a = rng.random(m * k) * 3 - 1
@@ -59,10 +65,30 @@ def test_reference_style_runner_with_concurrent_threads(workers, rng):
             for f in futs:
                 f.result()
         want = oracle.product(a, b, m, k, n, c, r)
-        if (c, r) == (2, 0):
+        if (c, r) == (2, 0) and tensor_cores:
             assert_within(res, want, sum_tolerance(k, a, b), f"{ops} W={workers}")
         else:
             assert_bits_equal(res, want, f"{ops} W={workers}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workers", [1, 4])
+def test_overwrite_variant_needs_no_prefill(workers, rng):
+    """product_rows_overwrite on an UNinitialised res (a _Runner branch that
+    skips the identity prefill) gives the bits of prefill + product_rows."""
+    mod = _module()
+    m, k, n = 130, 29, 77
+    a = rng.random(m * k) * 3 - 1
+    b = rng.random(k * n) * 3 - 1
+    for ops in (moa.MUL_ADD, moa.op_pair("add", "max"), moa.op_pair("multiply", "multiply")):
+        c, r = ops.codes()
+        res = np.empty(m * n)
+        res.fill(np.nan)  # garbage the overwrite must not read
+        with ThreadPoolExecutor(workers) as pool:
+            for f in [pool.submit(mod.product_rows_overwrite, res, a, b, m, k, n, k, n, n, c, r,
+                                  w, workers) for w in range(workers)]:
+                f.result()
+        assert_bits_equal(res, oracle.product(a, b, m, k, n, c, r), f"{ops} W={workers}")
 
 
 @pytest.mark.gpu

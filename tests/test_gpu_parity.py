@@ -45,9 +45,12 @@ def _run(case, exact=False, device=False, workers=1):
     return out.host_data()
 
 
+DMMA_MIN_K = 8  # capi.cu kDmmaMinK: below it (multiply, add) takes the exact fold
+
+
 def _is_dmma(case) -> bool:
     return case.comb == MUL and case.red == ADD and case.a.dtype == np.float64 and \
-        case.mode == "inner" and case.shape_a[-1] > 1
+        case.mode == "inner" and case.shape_a[-1] >= DMMA_MIN_K
 
 
 def _check(case, got, exact=False):
@@ -65,10 +68,100 @@ def _check(case, got, exact=False):
 
 
 def test_golden_cases_bitwise(golden_small):
+    """Every golden case on the default route, specials included: bit-exact,
+    except (multiply, add) float64 with K >= 8 (DMMA), within the sum bound."""
     for case in golden_small:
-        if _is_dmma(case) and case.tag.startswith("special"):
-            continue  # FMA vs separate rounding legitimately differ at overflow; see below
         _check(case, _run(case))
+
+
+def test_default_route_is_the_reference_below_one_dmma_k_group(golden_small):
+    """Every (multiply, add) float64 golden case with K < 8 — the reference's
+    special-value cases (NaN, +-inf, +-0, subnormals, +-1e308) among them —
+    is bit-exact on the default route, not just within tolerance."""
+    seen = 0
+    for case in golden_small:
+        if case.comb == MUL and case.red == ADD and case.a.dtype == np.float64 and \
+                case.mode == "inner" and 0 < case.shape_a[-1] < DMMA_MIN_K:
+            assert_bits_equal(_run(case), case.out, repr(case))
+            seen += 1
+    assert seen >= 15
+
+
+def _random_array(rng, rank, max_extent=5):
+    shape = tuple(int(e) for e in rng.integers(1, max_extent + 1, size=rank))
+    return MoaArray(shape, rng.random(math.prod(shape)) * 3.0 - 1.0)
+
+
+def test_criterion_1_oracle_equivalence_default_route():
+    """reference tests/test_acceptance.py:34-53 on the default (fast) routes:
+    1000 random cases over every built-in pair, half inner products of ranks
+    1..4 with extents 1..5, half outer products, values in [-1, 2); each
+    element within rtol 1e-12 (atol 0) of the oracle, min/max folds exact."""
+    rng = np.random.default_rng(1001)
+    pairs = list(moa.builtin_pairs())
+    for case in range(1000):
+        ops = pairs[case % len(pairs)]
+        comb, red = ops.codes()
+        if rng.random() < 0.5:
+            ra, rb = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+            shared = int(rng.integers(1, 6))
+            sa = tuple(int(e) for e in rng.integers(1, 6, size=ra - 1)) + (shared,)
+            sb = (shared,) + tuple(int(e) for e in rng.integers(1, 6, size=rb - 1))
+            a = MoaArray(sa, rng.random(math.prod(sa)) * 3.0 - 1.0)
+            b = MoaArray(sb, rng.random(math.prod(sb)) * 3.0 - 1.0)
+            got = moa.inner(a, b, ops)
+            m, k = math.prod(sa[:-1]), shared
+            n = math.prod(sb[1:])
+        else:
+            a = _random_array(rng, int(rng.integers(1, 5)))
+            b = _random_array(rng, int(rng.integers(1, 5)))
+            got = moa.outer(a, b, ops)
+            m, k, n = a.count, 1, b.count
+        want = oracle.product(a.data, b.data, m, k, n, comb, red)
+        if ops.reduce_name in ("min", "max"):
+            np.testing.assert_array_equal(got.data, want, err_msg=f"case {case} {ops}")
+        else:
+            np.testing.assert_allclose(got.data, want, rtol=1e-12, atol=0.0, equal_nan=True,
+                                       err_msg=f"case {case} {ops}")
+
+
+def _special_operand(rng, size, span):
+    """Uniform [-1, 1) with NaN, +-inf, +-0 and subnormals, each at rate 1/span."""
+    x = rng.uniform(-1.0, 1.0, size)
+    kinds = rng.integers(0, span, size)
+    x[kinds == 0] = np.nan
+    x[kinds == 1] = np.inf
+    x[kinds == 2] = -np.inf
+    x[kinds == 3] = 0.0
+    x[kinds == 4] = -0.0
+    sub = kinds == 5
+    x[sub] = rng.uniform(-1, 1, int(sub.sum())) * 2.0**-1060  # subnormal
+    return x
+
+
+@pytest.mark.parametrize("mkn", [(96, 8, 40),       # smallest DMMA K
+                                 (200, 64, 136),    # 16x32 TMA tiles
+                                 (2048, 48, 512),   # 64x64 TMA tiles
+                                 (301, 37, 203)])   # unaligned: cp.async kernel
+def test_dmma_route_ieee_specials(mkn, rng):
+    """The FP64 tensor-core route on NaN, +-inf, +-0 and subnormal operands:
+    the same NaN positions and the same infinities (signs included) as the
+    reference's loop, finite elements within K*2^-52*max|A|*max|B| over the
+    finite operands.  The one exception is overflow near DBL_MAX (the fused
+    DMMA step does not overflow where the reference's separate product does),
+    so values near 1e308 stay out of this set; include/moa_b200.h says so."""
+    m, k, n = mkn
+    for span in (600, 40):  # sparse specials (mostly finite results), dense
+        a = _special_operand(rng, m * k, span)
+        b = _special_operand(rng, k * n, span)
+        assert moa.kernel._native.plan_kernel(0, m, k, n, MUL, ADD) == "dmma"
+        got = moa.inner(MoaArray((m, k), a), MoaArray((k, n), b)).data
+        want = oracle.product(a, b, m, k, n, MUL, ADD)
+        fa, fb = a[np.isfinite(a)], b[np.isfinite(b)]
+        assert_within(got, want, sum_tolerance(k, fa, fb), f"{mkn} span {span}")
+        assert np.isnan(want).any()
+        if span == 600:
+            assert np.isfinite(want).mean() > 0.3
 
 
 def test_golden_cases_exact_mode_bitwise_everywhere(golden_small):
@@ -1024,7 +1117,10 @@ def test_int32_tropical_tma_route_wraps(k, lstride, rng):
 
 
 @pytest.mark.parametrize("mkn", [(700, 1000, 520),    # cp.async kernels
-                                 (2000, 1000, 520)])  # TMA kernel (>= 148 64x64 tiles)
+                                 (2000, 1000, 520),   # TMA kernel (>= 148 64x64 tiles)
+                                 (2000, 33, 520)])    # chunks 16+17: a 1-wide tail joins
+                                                      # its neighbour (else it would take
+                                                      # the outer route's rounding)
 def test_k_chunked_accumulation_replays_one_pass(mkn, rng):
     """Accumulating k-chunks (slab-aligned) with MOA_FLAG_ACCUMULATE gives the
     bits of one DMMA pass — what the pipelined broadcast of B relies on."""

@@ -311,13 +311,15 @@ def test_bench_job_plans_match_rank_blocks():
 
 def test_k_chunks_align_to_the_dmma_slab():
     from paper_0907_0792_b200.distributed import k_chunks
-    for K in (1, 15, 16, 17, 256, 16384, 1000):
+    for K in (1, 15, 16, 17, 33, 256, 16384, 1000, 1025):
         for n in (1, 2, 3, 8):
             ch = k_chunks(K, n)
             assert ch[0][0] == 0 and ch[-1][1] == K
             assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
             assert all(k0 % 16 == 0 for k0, _ in ch)
             assert len(ch) <= max(1, n)
+            # no short tail: every chunk keeps the whole product's route
+            assert len(ch) == 1 or all(k1 - k0 >= 16 for k0, k1 in ch)
 
 
 def test_launch_host_validates_before_the_abi():
