@@ -38,6 +38,7 @@
 #ifndef MOA_B200_H
 #define MOA_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -129,6 +130,20 @@ int moa_product_rows_host(int dtype, void* res, const void* a, const void* b,
                           int combine_code, int reduce_code,
                           int64_t start, int64_t step,
                           uint32_t flags, int device);
+
+/*
+ * Host memory for results (auxiliary; the reference has no counterpart — its
+ * _Runner allocates res with np.full, kernel.py:149).  moa_host_alloc returns
+ * `bytes` (rounded up to 2 MiB) of host memory backed by transparent huge
+ * pages, first-touched by the library's copy threads and page-locked with
+ * cudaHostRegister, so moa_product_rows_host writes results into it at link
+ * speed without staging.  moa_host_free returns it to a process-wide cache of
+ * idle blocks (reused by later allocations of a similar size; beyond
+ * $MOA_HOST_CACHE_BYTES, default 4 GiB, the oldest are unregistered and
+ * unmapped).  NULL on failure.  The memory is uninitialised.  Thread-safe.
+ */
+void* moa_host_alloc(size_t bytes);
+void moa_host_free(void* p);
 
 /* Message for the last failing call on this thread ("" if none). */
 const char* moa_last_error(void);

@@ -24,7 +24,8 @@ FLAG_EXACT = 2
 
 # every symbol include/moa_b200.h declares
 EXPORTS = ("moa_product_rows", "moa_product_rows_host", "moa_last_error", "moa_abi_version",
-           "moa_device_count", "moa_launch_count", "moa_plan_kernel")
+           "moa_device_count", "moa_launch_count", "moa_plan_kernel", "moa_host_alloc",
+           "moa_host_free")
 
 _lock = threading.Lock()
 _lib: ctypes.CDLL | None = None
@@ -52,6 +53,10 @@ def _bind(lib: ctypes.CDLL) -> None:
     lib.moa_device_count.argtypes = []
     lib.moa_launch_count.restype = ctypes.c_uint64
     lib.moa_launch_count.argtypes = []
+    lib.moa_host_alloc.restype = ctypes.c_void_p
+    lib.moa_host_alloc.argtypes = [ctypes.c_size_t]
+    lib.moa_host_free.restype = None
+    lib.moa_host_free.argtypes = [ctypes.c_void_p]
     lib.moa_plan_kernel.restype = ctypes.c_char_p
     lib.moa_plan_kernel.argtypes = [ctypes.c_int, _i64, _i64, _i64, ctypes.c_int,
                                     ctypes.c_int, ctypes.c_uint32]
@@ -125,6 +130,16 @@ def plan_kernel(dtype: int, noproc: int, rowsinred: int, elsinop: int,
                 combine_code: int, reduce_code: int, flags: int = 0) -> str:
     return load().moa_plan_kernel(dtype, noproc, rowsinred, elsinop, combine_code,
                                   reduce_code, flags).decode()
+
+
+def host_alloc(nbytes: int) -> int:
+    """moa_host_alloc: page-locked, huge-page-backed host memory (0 on failure)."""
+    return int(load().moa_host_alloc(nbytes) or 0)
+
+
+def host_free(ptr: int) -> None:
+    if _lib is not None:
+        _lib.moa_host_free(ptr)
 
 
 def launch_count() -> int:

@@ -24,6 +24,8 @@
 // events and small device buffers come from a per-device pool of queue sets
 // (one per concurrent caller), large block buffers from a private device
 // memory pool, so a call costs a few API calls beyond its copies and kernels.
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -112,6 +114,24 @@ std::vector<std::pair<int64_t, int64_t>> k_chunks(int64_t K, int chunks, int64_t
   return out;
 }
 
+// $MOA_HOST_TRACE=1: one stderr line per call with the host-side phase times
+struct Trace {
+  const bool on = std::getenv("MOA_HOST_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  std::string line;
+  void mark(const char* what) {
+    if (!on) return;
+    const double ms = std::chrono::duration<double, std::milli>(
+                          std::chrono::steady_clock::now() - t0).count();
+    char buf[64];
+    snprintf(buf, sizeof buf, " %s=%.3f", what, ms);
+    line += buf;
+  }
+  ~Trace() {
+    if (on) fprintf(stderr, "[moa_host]%s\n", line.c_str());
+  }
+};
+
 // one call's resources: a pooled queue set (returned at the end) and the
 // block buffers drawn from the device's private pool
 struct Session {
@@ -187,6 +207,7 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   const size_t esz = (dtype == MOA_DTYPE_F64 || dtype == MOA_DTYPE_I64) ? 8 : 4;
   const int64_t rows = (noproc - start + step - 1) / step;
 
+  Trace tr;
   Session ss;
   ss.device = device;
   int cur = 0;
@@ -205,6 +226,7 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     if (ss.pool == nullptr) return fail_cuda(e, "device memory pool");
   }
   moa::host::Queues& q = *ss.q;
+  tr.mark("setup");
 
   // A rows of the set pack densely (lda = K) when the set's rows do not
   // overlap; otherwise the whole span of A goes over with its own strides
@@ -236,11 +258,18 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   const int64_t lda = a_dense ? K : lstride * step, ldb = b_dense ? N : rstride;
 
   // A of the set (dense rows, or the whole strided span), B, onto the device
+  // (a column range [k0, k1) of a block's rows lands chunk-major: the nr x
+  // (k1-k0) panel densely at element nr*k0, so its device copy is one
+  // contiguous run — row-wise 2-D copies of narrow rows cost the copy engine
+  // ~2 us per row — and the chunk's kernel reads it with lda = k1 - k0)
   auto copy_a = [&](char* dst, int64_t r0, int64_t nr, int64_t k0, int64_t k1, cudaStream_t st) {
-    if (a_dense)
-      ss.check(moa::host::h2d(device, dst + (size_t)k0 * esz, (size_t)K * esz,
+    if (a_dense && k1 - k0 < K)
+      ss.check(moa::host::h2d(device, dst + (size_t)(nr * k0) * esz, (size_t)(k1 - k0) * esz,
                               a_rows + (size_t)r0 * a_pitch + (size_t)k0 * esz, a_pitch,
                               (size_t)(k1 - k0) * esz, (size_t)nr, a_pin, st));
+    else if (a_dense)
+      ss.check(moa::host::h2d(device, dst, (size_t)K * esz, a_rows + (size_t)r0 * a_pitch, a_pitch,
+                              (size_t)K * esz, (size_t)nr, a_pin, st));
     else
       ss.check(moa::host::h2d(device, dst, (size_t)a_span * esz, a_rows, (size_t)a_span * esz,
                               (size_t)a_span * esz, 1, a_pin, st));
@@ -270,6 +299,7 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
       ss.check(moa::host::h2d(device, c_dev, (size_t)N * esz, c_rows, c_pitch, (size_t)N * esz,
                               (size_t)rows, r_pin, st));
     if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product (copy in)");
+    tr.mark("in");
     const int rc = moa_product_rows(dtype, c_dev, K > 0 ? a_dev : nullptr, K > 0 ? b_dev : nullptr,
                                     rows, K, N, K > 0 ? lda : 0, K > 0 ? ldb : N, N, combine_code,
                                     reduce_code, 0, 1, flags, st);
@@ -277,6 +307,7 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
       ss.err = cudaErrorUnknown;  // drain before the queues are reused; message already set
       return rc;
     }
+    tr.mark("launched");
     const size_t out_bytes = (size_t)(rows * N) * esz;
     if (r_pin && rows >= 4 && out_bytes >= (64ull << 20)) {
       // a large result leaves over four copy queues, which draw a little
@@ -299,6 +330,7 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
                               (size_t)rows, r_pin, st));
       ss.check(cudaStreamSynchronize(st));
     }
+    tr.mark(r_pin ? "out_pinned" : "out_staged");
     if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product");
     return 0;
   }
@@ -374,31 +406,46 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     }
     cudaEvent_t a_ready = ss.event();
     ss.check(cudaEventRecord(a_ready, q.s_in));
-    if (i == 0 && K > 0) {
-      for (const auto& ch : chunks) {
-        if (a_by_chunk) copy_a(a_buf[slot], bl.r0, nr, ch.first, ch.second, q.s_in);
-        copy_b(b_buf, b_dense ? ch.first : 0, b_dense ? ch.second : K, q.s_in);
-        b_ready.push_back(ss.event());
-        ss.check(cudaEventRecord(b_ready.back(), q.s_in));
-      }
-    }
-    // --- compute
+    // --- compute, interleaved with B's chunks for the first block: each
+    // chunk's kernel is issued as soon as its copies are, so a staged (host-
+    // driven) transfer of B overlaps the chunks already computing
     ss.check(cudaStreamWaitEvent(q.s_comp, a_ready, 0));
     if (!acc && c_free[slot]) ss.check(cudaStreamWaitEvent(q.s_comp, c_free[slot], 0));
     if (ss.err != cudaSuccess) break;
     const bool per_chunk = i == 0 && chunks.size() > 1;
+    auto launch = [&](int64_t k0, int64_t k1, bool accumulate) {
+      const uint32_t f = (flags & ~MOA_FLAG_ACCUMULATE) | (accumulate ? MOA_FLAG_ACCUMULATE : 0u);
+      // a_by_chunk: the chunk's A panel is dense at element nr*k0 (copy_a)
+      const char* a_ptr = a_by_chunk ? a_buf[slot] + (size_t)(nr * k0) * esz
+                                     : a_buf[slot] + (size_t)k0 * esz;
+      return moa_product_rows(dtype, c_buf[slot], a_ptr, b_buf + (size_t)(k0 * ldb) * esz, nr,
+                              k1 - k0, N, a_by_chunk ? k1 - k0 : lda, ldb, N, combine_code,
+                              reduce_code, 0, 1, f, q.s_comp);
+    };
     if (K > 0) {
-      for (size_t j = 0; j < (per_chunk ? chunks.size() : 1); j++) {
+      if (i == 0) {
+        for (size_t j = 0; j < chunks.size(); j++) {
+          const auto& ch = chunks[j];
+          if (a_by_chunk) copy_a(a_buf[slot], bl.r0, nr, ch.first, ch.second, q.s_in);
+          copy_b(b_buf, b_dense ? ch.first : 0, b_dense ? ch.second : K, q.s_in);
+          b_ready.push_back(ss.event());
+          ss.check(cudaEventRecord(b_ready.back(), q.s_in));
+          if (per_chunk) {
+            ss.check(cudaStreamWaitEvent(q.s_comp, b_ready.back(), 0));
+            if (ss.err != cudaSuccess) break;
+            if (const int rc = launch(ch.first, ch.second, acc || j > 0); rc != 0) {
+              ss.err = cudaErrorUnknown;  // drain; message already set
+              return rc;
+            }
+          }
+        }
+      }
+      if (!per_chunk) {
         // blocks after the first read all of B: wait for its last chunk
-        ss.check(cudaStreamWaitEvent(q.s_comp, per_chunk ? b_ready[j] : b_ready.back(), 0));
-        const int64_t k0 = per_chunk ? chunks[j].first : 0, k1 = per_chunk ? chunks[j].second : K;
-        const uint32_t f = (flags & ~MOA_FLAG_ACCUMULATE) |
-                           ((acc || (per_chunk && j > 0)) ? MOA_FLAG_ACCUMULATE : 0u);
-        const int rc = moa_product_rows(dtype, c_buf[slot], a_buf[slot] + (size_t)k0 * esz,
-                                        b_buf + (size_t)(k0 * ldb) * esz, nr, k1 - k0, N, lda,
-                                        ldb, N, combine_code, reduce_code, 0, 1, f, q.s_comp);
-        if (rc != 0) {
-          ss.err = cudaErrorUnknown;  // drain; message already set
+        ss.check(cudaStreamWaitEvent(q.s_comp, b_ready.back(), 0));
+        if (ss.err != cudaSuccess) break;
+        if (const int rc = launch(0, K, acc); rc != 0) {
+          ss.err = cudaErrorUnknown;
           return rc;
         }
       }
@@ -415,12 +462,17 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     a_free[slot] = done[i];
     // --- out: the previous block's rows (issued after this block's kernel,
     // so a staged copy into pageable memory runs while the GPU computes)
-    if (i > 0) copy_out(i - 1);
+    tr.mark("blk_issued");
+    if (i > 0) {
+      copy_out(i - 1);
+      tr.mark("blk_out");
+    }
   }
   if (ss.err == cudaSuccess) copy_out(blocks.size() - 1);
   if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_out));
   if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_comp));
   if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_in));
+  tr.mark("end");
   if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product");
   return 0;
 }

@@ -3,12 +3,20 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
 #include <thread>
+#include <unordered_map>
+
+#include <emmintrin.h>
+#include <sys/mman.h>
+
+#include "../../include/moa_b200.h"
 
 namespace moa::host {
 namespace {
@@ -93,9 +101,15 @@ Workers& workers() {
 }
 
 // -------------------------------------------------------------- per device
-constexpr size_t kSlotBytes = 8ull << 20;
-constexpr int kMaxSlots = 32;         // <= 256 MiB of page-locked staging per GPU
-constexpr int kSlotsPerTransfer = 6;  // 48 MiB in flight per copy
+// staging geometry: slot size and slots per transfer ($MOA_HOST_SLOT_MB,
+// $MOA_HOST_SLOTS override them); at most 256 MiB of slots per GPU
+size_t env_or(const char* name, size_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? (size_t)std::strtoull(e, nullptr, 10) : dflt;
+}
+const size_t kSlotBytes = env_or("MOA_HOST_SLOT_MB", 16) << 20;
+const int kSlotsPerTransfer = (int)env_or("MOA_HOST_SLOTS", 4);
+const int kMaxSlots = (int)std::max<size_t>(kSlotsPerTransfer, (256ull << 20) / kSlotBytes);
 constexpr size_t kDirectBytes = 256ull << 10;
 constexpr size_t kCacheLimit = 16ull << 20;  // per cached device buffer
 
@@ -183,12 +197,39 @@ std::vector<Chunk> chunks_of(size_t width, size_t rows) {
   return out;
 }
 
+// Copy into a staging slot with non-temporal (streaming) stores.  The copy
+// engine reads the slot right after the threads write it; lines left dirty in
+// the 16 cores' private caches make those DMA reads snoop-bound — 7 GB/s
+// instead of 54 GB/s for a 16 MiB slot packed by 16 threads
+// (tools/host_probe.cu, profiles/r02_host_probe.json) — so the packed data
+// goes straight to memory instead.
+void stream_copy(char* dst, const char* src, size_t n) {
+  size_t head = (16 - reinterpret_cast<uintptr_t>(dst) % 16) % 16;
+  if (head > n) head = n;
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  const size_t body = n / 64 * 64;
+  for (size_t i = 0; i < body; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  std::memcpy(dst + body, src + body, n - body);
+}
+
 // copy a chunk between the slot (dense, pitch cw) and host rows (pitch hp),
-// split over the copy threads in ~512 KiB pieces
+// split over the copy threads in >= 1 MiB pieces
 void pack(char* slot, const char* host, size_t hp, const Chunk& ch, bool to_slot) {
   const size_t total = ch.nr * ch.cw;
   const int pieces = (int)std::min<size_t>(
-      (size_t)workers().size() + 1, std::max<size_t>(1, total / (512ull << 10)));
+      (size_t)workers().size() + 1, std::max<size_t>(1, total / (1ull << 20)));
   const size_t per = (total + pieces - 1) / pieces;
   parallel_for(pieces, [&](int p) {
     size_t b = (size_t)p * per;
@@ -198,14 +239,35 @@ void pack(char* slot, const char* host, size_t hp, const Chunk& ch, bool to_slot
       const size_t n = std::min(ch.cw - c, e - b);
       char* s = slot + b;
       char* h = const_cast<char*>(host) + (ch.r0 + r) * hp + ch.c0 + c;
+      // streaming stores into a slot (see stream_copy); plain stores into the
+      // caller's rows (streaming them measured no faster)
       if (to_slot)
-        std::memcpy(s, h, n);
+        stream_copy(s, h, n);
       else
         std::memcpy(h, s, n);
       b += n;
     }
+    if (to_slot) _mm_sfence();  // streaming stores visible before the copy is issued
   });
 }
+
+// $MOA_HOST_TRACE: per staged transfer, time packing vs waiting for slots
+struct StageTrace {
+  const bool on = std::getenv("MOA_HOST_TRACE") != nullptr;
+  double pack_ms = 0, wait_ms = 0;
+  size_t bytes = 0;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  const char* dir;
+  explicit StageTrace(const char* d) : dir(d) {}
+  static double since(std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+  }
+  ~StageTrace() {
+    if (on && bytes)
+      fprintf(stderr, "[moa_stage] %s %.1f MiB total=%.2f ms pack=%.2f wait=%.2f -> %.1f GB/s\n", dir,
+              bytes / 1048576.0, since(t0), pack_ms, wait_ms, bytes / since(t0) / 1e6);
+  }
+};
 
 }  // namespace
 
@@ -323,14 +385,22 @@ cudaError_t h2d(int device, void* dst, size_t dpitch, const void* src, size_t hp
       acquire(device, (int)std::min<size_t>(kSlotsPerTransfer, chunks.size()), err);
   if (slots.empty()) return err != cudaSuccess ? err : cudaErrorMemoryAllocation;
   const size_t d = slots.size();
+  StageTrace tr("h2d");
+  tr.bytes = width * rows;
   for (size_t c = 0; c < chunks.size() && err == cudaSuccess; c++) {
     Slot& s = slots[c % d];
+    auto t = std::chrono::steady_clock::now();
     if (c >= d) err = cudaEventSynchronize(s.ev);  // its previous chunk has left
+    tr.wait_ms += StageTrace::since(t);
     if (err != cudaSuccess) break;
     const Chunk& ch = chunks[c];
+    t = std::chrono::steady_clock::now();
     pack(s.ptr, static_cast<const char*>(src), hpitch, ch, true);
-    err = cudaMemcpy2DAsync(static_cast<char*>(dst) + ch.r0 * dpitch + ch.c0, dpitch, s.ptr,
-                            ch.cw, ch.cw, ch.nr, cudaMemcpyHostToDevice, st);
+    tr.pack_ms += StageTrace::since(t);
+    char* d = static_cast<char*>(dst) + ch.r0 * dpitch + ch.c0;
+    err = dpitch == ch.cw
+              ? cudaMemcpyAsync(d, s.ptr, ch.cw * ch.nr, cudaMemcpyHostToDevice, st)
+              : cudaMemcpy2DAsync(d, dpitch, s.ptr, ch.cw, ch.cw, ch.nr, cudaMemcpyHostToDevice, st);
     if (err == cudaSuccess) err = cudaEventRecord(s.ev, st);
   }
   release(device, slots);  // the next user of a slot waits for its event
@@ -356,17 +426,26 @@ cudaError_t d2h(int device, void* dst, size_t hpitch, const void* src, size_t dp
   auto issue = [&](size_t c) {
     const Chunk& ch = chunks[c];
     Slot& s = slots[c % d];
-    cudaError_t e = cudaMemcpy2DAsync(s.ptr, ch.cw, static_cast<const char*>(src) + ch.r0 * dpitch + ch.c0,
-                                      dpitch, ch.cw, ch.nr, cudaMemcpyDeviceToHost, st);
+    const char* d = static_cast<const char*>(src) + ch.r0 * dpitch + ch.c0;
+    cudaError_t e = dpitch == ch.cw
+                        ? cudaMemcpyAsync(s.ptr, d, ch.cw * ch.nr, cudaMemcpyDeviceToHost, st)
+                        : cudaMemcpy2DAsync(s.ptr, ch.cw, d, dpitch, ch.cw, ch.nr,
+                                            cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaEventRecord(s.ev, st);
     if (e != cudaSuccess && err == cudaSuccess) err = e;
   };
   for (size_t c = 0; c < d && c < chunks.size(); c++) issue(c);
+  StageTrace tr("d2h");
+  tr.bytes = width * rows;
   for (size_t c = 0; c < chunks.size() && err == cudaSuccess; c++) {
     Slot& s = slots[c % d];
+    auto t = std::chrono::steady_clock::now();
     err = cudaEventSynchronize(s.ev);
+    tr.wait_ms += StageTrace::since(t);
     if (err != cudaSuccess) break;
+    t = std::chrono::steady_clock::now();
     pack(s.ptr, static_cast<const char*>(dst), hpitch, chunks[c], false);
+    tr.pack_ms += StageTrace::since(t);
     if (c + d < chunks.size()) issue(c + d);
   }
   if (err != cudaSuccess) cudaStreamSynchronize(st);  // no copy may still target a slot
@@ -375,3 +454,116 @@ cudaError_t d2h(int device, void* dst, size_t hpitch, const void* src, size_t dp
 }
 
 }  // namespace moa::host
+
+// ------------------------------------------------------- host result blocks
+namespace moa::host {
+namespace {
+
+constexpr size_t kHugePage = 2ull << 20;
+
+struct HostBlock {
+  char* map = nullptr;  // the mapping (one huge page longer, for alignment)
+  size_t map_bytes = 0;
+  char* ptr = nullptr;  // 2 MiB aligned
+  size_t bytes = 0;
+  bool registered = false;
+};
+
+struct HostCache {
+  std::mutex mu;
+  std::unordered_map<void*, HostBlock> live;
+  std::deque<HostBlock> idle;  // oldest first
+  size_t idle_bytes = 0;
+};
+
+HostCache& host_cache() {
+  static HostCache* c = new HostCache();
+  return *c;
+}
+
+size_t host_cache_cap() {
+  static const size_t cap = [] {
+    if (const char* e = std::getenv("MOA_HOST_CACHE_BYTES")) return (size_t)std::strtoull(e, nullptr, 10);
+    return (size_t)(4ull << 30);
+  }();
+  return cap;
+}
+
+void destroy(HostBlock& b) {
+  if (b.registered) {
+    cudaHostUnregister(b.ptr);
+    (void)cudaGetLastError();
+  }
+  munmap(b.map, b.map_bytes);
+}
+
+}  // namespace
+}  // namespace moa::host
+
+extern "C" void* moa_host_alloc(size_t bytes) {
+  using namespace moa::host;
+  if (bytes == 0) bytes = 1;
+  const size_t size = (bytes + kHugePage - 1) / kHugePage * kHugePage;
+  HostCache& hc = host_cache();
+  {
+    // reuse the smallest idle block that fits without wasting over a quarter
+    std::lock_guard<std::mutex> lk(hc.mu);
+    auto best = hc.idle.end();
+    for (auto it = hc.idle.begin(); it != hc.idle.end(); ++it)
+      if (it->bytes >= size && it->bytes <= size + size / 4 &&
+          (best == hc.idle.end() || it->bytes < best->bytes))
+        best = it;
+    if (best != hc.idle.end()) {
+      HostBlock b = *best;
+      hc.idle.erase(best);
+      hc.idle_bytes -= b.bytes;
+      hc.live[b.ptr] = b;
+      return b.ptr;
+    }
+  }
+  HostBlock b;
+  b.map_bytes = size + kHugePage;
+  void* m = mmap(nullptr, b.map_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (m == MAP_FAILED) return nullptr;
+  b.map = static_cast<char*>(m);
+  b.ptr = b.map + ((kHugePage - reinterpret_cast<uintptr_t>(b.map) % kHugePage) % kHugePage);
+  b.bytes = size;
+  madvise(b.ptr, size, MADV_HUGEPAGE);
+  // first touch by the copy threads, each a contiguous run of huge pages
+  // (~60 GB/s on a 16-core B200 host vs ~10 GB/s from one thread)
+  const size_t pages = size / kHugePage;
+  const int parts = (int)std::min<size_t>(pages, (size_t)copy_threads());
+  parallel_for(parts, [&](int p) {
+    const size_t p0 = pages * p / parts, p1 = pages * (p + 1) / parts;
+    for (size_t i = p0 * kHugePage; i < p1 * kHugePage; i += 4096) b.ptr[i] = 0;
+  });
+  // page-lock it once; from then on device copies into it run at link speed
+  // with no staging (cudaHostRegister of faulted memory: ~18 ms per GiB, vs
+  // ~390 ms per GiB for cudaHostAlloc)
+  b.registered = cudaHostRegister(b.ptr, size, cudaHostRegisterPortable) == cudaSuccess;
+  if (!b.registered) (void)cudaGetLastError();  // stays usable, staged
+  std::lock_guard<std::mutex> lk(hc.mu);
+  hc.live[b.ptr] = b;
+  return b.ptr;
+}
+
+extern "C" void moa_host_free(void* p) {
+  using namespace moa::host;
+  if (p == nullptr) return;
+  HostCache& hc = host_cache();
+  std::vector<HostBlock> evict;
+  {
+    std::lock_guard<std::mutex> lk(hc.mu);
+    auto it = hc.live.find(p);
+    if (it == hc.live.end()) return;
+    hc.idle.push_back(it->second);
+    hc.idle_bytes += it->second.bytes;
+    hc.live.erase(it);
+    while (hc.idle_bytes > host_cache_cap() && !hc.idle.empty()) {
+      evict.push_back(hc.idle.front());
+      hc.idle_bytes -= hc.idle.front().bytes;
+      hc.idle.pop_front();
+    }
+  }
+  for (HostBlock& b : evict) destroy(b);
+}

@@ -19,9 +19,10 @@ start, start+step, ... on the current CUDA stream.
 
 from __future__ import annotations
 
+import ctypes
 import enum
-import mmap
 import warnings
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -351,26 +352,26 @@ _HUGE_PAGE = 2 << 20
 
 
 def host_empty(n: int, dtype) -> np.ndarray:
-    """Uninitialised PAGEABLE host memory for a result of ``n`` elements.
+    """Uninitialised host memory for a result of ``n`` elements.
 
-    Large results are anonymous mappings aligned to and advised for 2 MiB
-    transparent huge pages: the executor's copy threads first-touch them while
-    staging the result back (512x fewer page faults than 4 KiB pages; a fresh
-    1 GiB result fills at ~45 GB/s with 16 threads on a B200 host,
-    profiles/r02_host_probe.json), and no page-locked allocation — 0.39 s per
-    GiB through the driver — is ever made per call."""
+    Large results come from the library's host block cache
+    (``moa_host_alloc``): huge-page-backed, first-touched by its copy threads
+    and page-locked with cudaHostRegister (~40 ms per GiB the first time,
+    against 0.39 s per GiB for cudaHostAlloc on a B200 host,
+    profiles/r02_host_probe.json), so the result's copy-back runs at link
+    speed; when the array is garbage-collected the block returns to the cache
+    and the next result of a similar size reuses it.  Small results are plain
+    numpy memory."""
     dt = np.dtype(dtype)
     nbytes = n * dt.itemsize
     if nbytes < 2 * _HUGE_PAGE:
         return np.empty(n, dt)
-    mm = mmap.mmap(-1, nbytes + _HUGE_PAGE)
-    base = np.frombuffer(mm, dtype=np.uint8, count=1).ctypes.data
-    off = (-base) % _HUGE_PAGE
-    try:
-        mm.madvise(mmap.MADV_HUGEPAGE, off, nbytes)
-    except (AttributeError, OSError, ValueError):  # pragma: no cover - kernel without THP
-        pass
-    return np.frombuffer(mm, dtype=dt, count=n, offset=off)
+    ptr = _native.host_alloc(nbytes)
+    if not ptr:  # pragma: no cover - host out of memory
+        return np.empty(n, dt)
+    buf = (ctypes.c_char * nbytes).from_address(ptr)
+    weakref.finalize(buf, _native.host_free, ptr)
+    return np.frombuffer(buf, dtype=dt, count=n)
 
 
 def execute_host(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair = MUL_ADD, *,

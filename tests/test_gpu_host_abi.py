@@ -291,3 +291,29 @@ def test_short_lived_threads_reuse_pooled_queues(rng):
             list(pool.map(lambda w: launch_host(plan, res, a, b, op_pair("multiply", "max"),
                                                 start=w, step=4), range(4)))
         assert_bits_equal(res, want)
+
+
+def test_host_result_blocks_are_page_locked_and_reused(rng):
+    """Public-API results above 4 MiB live in moa_host_alloc blocks: huge-page
+    backed and page-locked (the copy-back needs no staging), returned to the
+    cache when the array dies and reused by the next result of that size."""
+    import gc
+    torch = _torch()
+    from paper_0907_0792_b200 import MoaArray, _native
+    x, y = rng.random(1000) * 2 - 1, rng.random(3000) * 2 - 1
+    out = moa.outer(MoaArray((1000,), x), MoaArray((3000,), y))
+    assert_bits_equal(out.data, (np.multiply.outer(x, y) + 0.0).ravel())
+    ptr = out.data.ctypes.data
+    assert ptr % (2 << 20) == 0
+    t = torch.from_numpy(out.data)
+    assert t.is_pinned()  # registered with CUDA
+    del out, t
+    gc.collect()
+    out2 = moa.outer(MoaArray((1000,), y[:1000]), MoaArray((3000,), y))
+    assert out2.data.ctypes.data == ptr  # the idle block was reused
+    assert_bits_equal(out2.data, (np.multiply.outer(y[:1000], y) + 0.0).ravel())
+    # the raw allocator: distinct live blocks, reuse after free
+    p1, p2 = _native.host_alloc(5 << 20), _native.host_alloc(5 << 20)
+    assert p1 and p2 and p1 != p2
+    _native.host_free(p1)
+    assert _native.host_alloc(5 << 20) == p1

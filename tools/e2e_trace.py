@@ -1,7 +1,9 @@
 """Timeline of one end-to-end (host buffers in, host result out) product of a
 BASELINE config through the public API, from a torch.profiler (CUPTI) trace:
 per-stream busy time of H2D copies, kernels and D2H copies, and the span
-(tools probe; not a test).  Usage: python tools/e2e_trace.py c5 [out.json]"""
+(tools probe; not a test).  Usage: python tools/e2e_trace.py c5 [out.json] [pageable]
+("pageable": plain numpy inputs and a prefaulted numpy result through the C
+ABI, i.e. the staged path)"""
 
 import json
 import sys
@@ -28,10 +30,21 @@ def pinned(x):
     return t
 
 
-ap, bp = pinned(a), pinned(b)
-A = MoaArray._wrap(w.shape_a, ap.numpy())
-B = MoaArray._wrap(w.shape_b, bp.numpy())
-fn = moa.inner if w.mode == "inner" else moa.outer
+pageable = len(sys.argv) > 3 and sys.argv[3] == "pageable"
+if pageable:
+    from paper_0907_0792_b200.kernel import launch_host, plan_inner, plan_outer
+    plan = (plan_inner if w.mode == "inner" else plan_outer)(w.shape_a, w.shape_b)
+    res = np.zeros(w.mkn[0] * w.mkn[2], dtype=a.dtype)
+
+    def fn(_a, _b, ops):
+        launch_host(plan, res, a, b, ops)
+        return res
+    A = B = None
+else:
+    ap, bp = pinned(a), pinned(b)
+    A = MoaArray._wrap(w.shape_a, ap.numpy())
+    B = MoaArray._wrap(w.shape_b, bp.numpy())
+    fn = moa.inner if w.mode == "inner" else moa.outer
 out = None
 for _ in range(2):
     out = None

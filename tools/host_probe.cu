@@ -3,6 +3,7 @@
 // pageable memcpy runs with T threads, what direct pageable cudaMemcpy
 // achieves, and what cudaHostRegister costs.  Prints one JSON object.
 // Build: nvcc -O2 -std=c++17 -o tools/host_probe tools/host_probe.cu -lpthread
+#include <emmintrin.h>
 #include <sys/mman.h>
 
 #include <chrono>
@@ -41,6 +42,12 @@ static void touch(char* d, const char*, size_t n) {
   for (size_t i = 0; i < n; i += 4096) d[i] = 1;
 }
 static void copy(char* d, const char* s, size_t n) { memcpy(d, s, n); }
+static void copy_nt(char* d, const char* s, size_t n) {  // d 16-byte aligned, n % 16 == 0
+  for (size_t i = 0; i < n; i += 16)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d + i),
+                     _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i)));
+  _mm_sfence();
+}
 
 static char* fresh(bool huge) {
   void* p = mmap(nullptr, kBytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
@@ -143,6 +150,80 @@ int main() {
     t0 = now();
     CK(cudaFreeHost(p2));
     add("cuda_free_host_1GiB_ms", (now() - t0) * 1e3);
+  }
+  // staging pack: prefaulted 4 KiB-page source (like a numpy array) into a
+  // ring of page-locked slots, T threads per slot
+  {
+    const size_t src_bytes = 2ull << 30;
+    char* src = static_cast<char*>(mmap(nullptr, src_bytes, PROT_READ | PROT_WRITE,
+                                        MAP_PRIVATE | MAP_ANONYMOUS, -1, 0));
+    madvise(src, src_bytes, MADV_NOHUGEPAGE);
+    par(16, src_bytes, touch, src, nullptr);
+    for (size_t slot_mb : {4, 16, 64}) {
+      const size_t slot = slot_mb << 20;
+      char* ring = nullptr;
+      CK(cudaHostAlloc((void**)&ring, 4 * slot, cudaHostAllocPortable));
+      for (int t : {4, 8, 16}) {
+        double t0 = now();
+        for (size_t off = 0, i = 0; off < src_bytes; off += slot, i++)
+          par(t, slot, copy, ring + (i % 4) * slot, src + off);
+        add("pack_4k_src_slot" + std::to_string(slot_mb) + "M_" + std::to_string(t) + "t_GBs",
+            src_bytes / (now() - t0) / 1e9);
+      }
+      CK(cudaFreeHost(ring));
+    }
+    // the same source advised for huge pages after the fact
+    madvise(src, src_bytes, MADV_HUGEPAGE);
+    munmap(src, src_bytes);
+  }
+  // DMA right after a CPU pack vs from a slot written long before: does the
+  // copy engine slow down on freshly written (cache-dirty) pinned lines?
+  {
+    const size_t slot = 16ull << 20;
+    char* ring = nullptr;
+    CK(cudaHostAlloc((void**)&ring, 4 * slot, cudaHostAllocPortable));
+    char* src = static_cast<char*>(malloc(256ull << 20));
+    memset(src, 5, 256ull << 20);
+    cudaStream_t st;
+    CK(cudaStreamCreate(&st));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    auto dma = [&](char* from) {
+      CK(cudaEventRecord(e0, st));
+      CK(cudaMemcpyAsync(dev, from, slot, cudaMemcpyHostToDevice, st));
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      return ms;
+    };
+    memset(ring, 1, 4 * slot);
+    float cold = 0, hot_contig = 0, hot_gather = 0;
+    for (int r = 0; r < 8; r++) cold += dma(ring + (r % 4) * slot);
+    for (int r = 0; r < 8; r++) {
+      char* sl = ring + (r % 4) * slot;
+      par(16, slot, copy, sl, src + r * slot);
+      hot_contig += dma(sl);
+    }
+    for (int r = 0; r < 8; r++) {  // 16 KiB pieces gathered from a 128 KiB pitch
+      char* sl = ring + (r % 4) * slot;
+      const size_t rows = slot / 16384;
+      for (size_t i = 0; i < rows; i++) memcpy(sl + i * 16384, src + (i * 131072) % (256ull << 20), 16384);
+      hot_gather += dma(sl);
+    }
+    float hot_nt = 0;
+    for (int r = 0; r < 8; r++) {  // the same contiguous pack with streaming stores
+      char* sl = ring + (r % 4) * slot;
+      par(16, slot, copy_nt, sl, src + r * slot);
+      hot_nt += dma(sl);
+    }
+    add("dma16M_after_contig_pack_nt_GBs", slot * 8 / (hot_nt * 1e-3) / 1e9);
+    add("dma16M_cold_slot_GBs", slot * 8 / (cold * 1e-3) / 1e9);
+    add("dma16M_after_contig_pack_GBs", slot * 8 / (hot_contig * 1e-3) / 1e9);
+    add("dma16M_after_gather_pack_GBs", slot * 8 / (hot_gather * 1e-3) / 1e9);
+    CK(cudaFreeHost(ring));
+    free(src);
   }
   out += "}";
   printf("%s\n", out.c_str());
