@@ -19,6 +19,8 @@ from __future__ import annotations
 
 from typing import Callable
 
+import numpy as np
+
 from .kernel import KernelPlan, d2h_split, launch
 from .ops import MUL_ADD, OpPair
 
@@ -150,16 +152,20 @@ def sharded_product(plan: KernelPlan, a_block, b, ops: OpPair = MUL_ADD, *, grou
         return c
     # pipelined: async, in-order broadcasts of B's k-chunks; compute chases them
     n, k = plan.elsinop, plan.rowsinred
+    b_all = torch.empty(k * n, dtype=a_block.dtype, device=a_block.device)
+    b_src = None
     if rank == src:
-        # B in A's dtype, so every rank's chunk broadcasts post equal byte counts
-        b_all = b.reshape(-1).to(device=a_block.device, dtype=a_block.dtype).contiguous()
-        if b_all.numel() != k * n:
-            raise ValueError(f"B holds {b_all.numel()} elements; the plan needs {k * n}")
-    else:
-        b_all = torch.empty(k * n, dtype=a_block.dtype, device=a_block.device)
+        b_src = b.reshape(-1)
+        if b_src.numel() != k * n:
+            raise ValueError(f"B holds {b_src.numel()} elements; the plan needs {k * n}")
     chunks = k_chunks(k, bcast_chunks, align)
-    works = [dist.broadcast(b_all[k0 * n:k1 * n], src=src, group=group, async_op=True)
-             for k0, k1 in chunks]
+    works = []
+    for k0, k1 in chunks:
+        if b_src is not None:
+            # src stages chunk by chunk (from host memory too), in A's dtype so
+            # every rank's broadcast of the chunk posts equal byte counts
+            b_all[k0 * n:k1 * n].copy_(b_src[k0 * n:k1 * n], non_blocking=True)
+        works.append(dist.broadcast(b_all[k0 * n:k1 * n], src=src, group=group, async_op=True))
     for i, ((k0, k1), work) in enumerate(zip(chunks, works)):
         work.wait()  # the current stream waits for this chunk only
         if sub.noproc:
@@ -189,17 +195,27 @@ def gather_rows(c_block, plan: KernelPlan, *, dst: int = 0, group=None):
 
 
 def sharded_product_host(plan: KernelPlan, a_block_host, b_host, ops: OpPair = MUL_ADD, *,
-                         device, group=None, src: int = 0, exact: bool = False):
-    """Host-buffer form of ``sharded_product``: copy this rank's A rows (and B on
-    ``src``) to ``device``, broadcast B, compute, and copy the result block back
-    to pinned host memory (returned as a numpy vector)."""
+                         device, group=None, src: int = 0, exact: bool = False,
+                         bcast_chunks: int = 8):
+    """Host-buffer form of ``sharded_product``: this rank's A rows go to
+    ``device``; on ``src`` B goes up in k-chunks, each broadcast as soon as it
+    is on the device and folded by every rank while later chunks are still in
+    flight (where the fold replays exactly, ``bcast_chunk_align``; else B goes
+    whole); the result block comes back into page-locked host memory
+    (``kernel.host_empty``), returned as a numpy vector."""
     torch = _torch()
+    from .kernel import host_empty
     a_dev = _to_device(a_block_host, device)
-    b_dev = _to_device(b_host, device) if b_host is not None else None
-    c = sharded_product(plan, a_dev, b_dev, ops, group=group, src=src, exact=exact)
-    out = torch.empty(c.numel(), dtype=c.dtype, pin_memory=True)
-    d2h_split(out, c, torch.cuda.current_stream(c.device))
-    return out.numpy()
+    b_arg = None
+    if b_host is not None:
+        b_arg = b_host if isinstance(b_host, torch.Tensor) else torch.from_numpy(b_host)
+        if not b_arg.is_cuda and bcast_chunk_align(ops, a_dev.dtype) is None:
+            b_arg = _to_device(b_arg, device)
+    c = sharded_product(plan, a_dev, b_arg, ops, group=group, src=src, exact=exact,
+                        bcast_chunks=bcast_chunks)
+    out = host_empty(c.numel(), np.dtype(str(c.dtype).replace("torch.", "")))
+    d2h_split(torch.from_numpy(out), c, torch.cuda.current_stream(c.device))
+    return out
 
 
 def _to_device(x, device):

@@ -1173,6 +1173,29 @@ def test_workers_over_repeated_devices_bitwise(rng):
             assert_bits_equal(got.host_data(), want)
 
 
+@pytest.mark.parametrize("chunks", [2, 3, 5])
+def test_execute_parallel_chunked_broadcast_schedule_bitwise(chunks, rng):
+    """The k-chunked schedule execute_parallel uses with several GPUs (B's
+    broadcast in k-chunks, each block's kernel accumulating chunk by chunk on
+    its own stream, chunk i waiting on chunk i's arrival event) reproduces one
+    launch bit for bit; on a one-GPU box the blocks share GPU 0 and the
+    broadcast itself is skipped, the chunk pipeline is not."""
+    m, k, n = 611, 260, 333
+    for ops, dt in ((moa.MUL_ADD, np.float64), (op_pair("add", "min"), np.float32),
+                    (op_pair("subtract", "max"), np.float64), (op_pair("divide", "max"), np.float64)):
+        a = MoaArray((m, k), rng.random(m * k) * 10 + 1, dtype=dt)
+        b = MoaArray((k, n), rng.random(k * n) * 10 + 1, dtype=dt)
+        plan = moa.plan_inner(a.shape, b.shape)
+        want = moa.execute_sequential(plan, a, b, ops).data
+        for devs in ([0, 0], [0, 0, 0]):
+            got = moa.execute_parallel(plan, a, b, ops, workers=len(devs), devices=devs,
+                                       bcast_chunks=chunks)
+            assert_bits_equal(got.data, want, f"{ops} {dt.__name__} {devs} chunks={chunks}")
+            got = moa.execute_parallel(plan, a.to_device(), b.to_device(), ops, workers=len(devs),
+                                       devices=devs, bcast_chunks=chunks)
+            assert_bits_equal(got.host_data(), want, f"{ops} {dt.__name__} device")
+
+
 def test_oracle_api_mirrors_reference_definitions(golden_small):
     """oracle_inner / oracle_outer (reference oracle.py:33-72) exported for API
     parity: inner = the exact fold, outer = combine with no reduce."""
