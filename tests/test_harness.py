@@ -171,3 +171,76 @@ def test_experiment_checksums_independent_of_workers_and_reproducible():
     r1, r2 = harness.run_experiment(cfg), harness.run_experiment(cfg)
     assert [r.checksum for r in r1.records] == [r.checksum for r in r2.records]
     assert all(r.threads == 2 and r.seconds > 0 for r in r1.records)
+
+
+# ---- against the reference harness's own records (tests/golden/harness_ref.json,
+# made by tests/golden/make_harness_golden.py from the imported reference) -------
+
+def _ref_harness():
+    import json
+    from conftest import GOLDEN
+    return json.loads((GOLDEN / "harness_ref.json").read_text())
+
+
+def _records_from_text(tmp_path, name, text):
+    p = tmp_path / f"{name}.csv"
+    p.write_text(text)
+    return read_records_csv(p)
+
+
+def test_reference_records_round_trip_and_metrics_identical(tmp_path):
+    """The reference's raw CSV parses with this harness and re-emits to the same
+    text; derive_metrics + emit_csv on the reference's own timings give the
+    reference's metric CSV text exactly (bench.py:180-247)."""
+    ref = _ref_harness()
+    for name, exp in ref.items():
+        if not isinstance(exp, dict):
+            continue
+        recs = _records_from_text(tmp_path, name, exp["raw_csv"])
+        again = tmp_path / f"{name}_again.csv"
+        emit_csv(again, recs)
+        assert again.read_text() == exp["raw_csv"], name
+        if exp["metrics_csv"] is not None:
+            m = tmp_path / f"{name}_m.csv"
+            emit_csv(m, derive_metrics(recs, [r for r in recs if r.threads == 1]), kind="metrics")
+            assert m.read_text() == exp["metrics_csv"], name
+    w1 = _records_from_text(tmp_path, "w1", ref["inner_w1"]["raw_csv"])
+    w2 = _records_from_text(tmp_path, "w2", ref["inner_w2"]["raw_csv"])
+    m = tmp_path / "w2w1.csv"
+    emit_csv(m, derive_metrics(w2, w1), kind="metrics")
+    assert m.read_text() == ref["metrics_w2_vs_w1"]
+
+
+@pytest.mark.gpu
+def test_harness_records_match_the_reference_harness(tmp_path):
+    """This harness run on the GPU with the reference's experiment configs:
+    identical CSV schema and row keys (mode, threads, ell, n, repeat);
+    checksums bit-identical for the exact folds (tropical, outer products,
+    (multiply, add) below K = 8) and within the north-star sum bound
+    K*2^-52*max|A|*max|B| per element for (multiply, add) on the tensor cores
+    and the cuBLAS comparator."""
+    ref = _ref_harness()
+    for name, exp in ref.items():
+        if not isinstance(exp, dict):
+            continue
+        cfg = ExperimentConfig(**exp["config"])
+        res = harness.run_experiment(cfg)
+        assert not res.failures
+        ours = tmp_path / f"{name}.csv"
+        emit_csv(ours, res.records)
+        assert ours.read_text().splitlines()[0] == exp["raw_csv"].splitlines()[0]
+        theirs = _records_from_text(tmp_path, f"{name}_ref", exp["raw_csv"])
+        mine = read_records_csv(ours)
+        assert [(r.mode, r.threads, r.ell, r.n, r.repeat) for r in mine] == \
+            [(r.mode, r.threads, r.ell, r.n, r.repeat) for r in theirs], name
+        rows = cfg.rows if cfg.rows is not None else cfg.workers
+        exact = (cfg.mode == "moa-outer" or (cfg.combine, cfg.reduce) != ("multiply", "add")
+                 or (cfg.mode == "moa-inner" and cfg.ell < 8))
+        for x, y in zip(mine, theirs):
+            if exact:
+                assert x.checksum == y.checksum, (name, x, y)
+            else:  # values in [0, 1): max|A| = max|B| <= 1
+                count = rows * x.n
+                tol = count * cfg.ell * 2.0**-52 + 4 * 2.0**-52 * abs(y.checksum) * \
+                    max(1.0, math.log2(count))
+                assert abs(x.checksum - y.checksum) <= tol, (name, x, y, tol)
