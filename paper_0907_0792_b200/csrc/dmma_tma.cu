@@ -30,21 +30,26 @@ namespace {
 // BM x BN CTA tile of (BM/WM)*(BN/WN) warps, WM x WN warp tiles (multiples of
 // 16: the relabelling works on 16-row blocks and pairs of n8 blocks), 16-deep
 // slabs in STAGES pipeline stages, MINB CTAs per SM, GM-row-tile raster groups
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, int GM_>
+// REFILL 0: thread 0 refills a stage once every warp has released it (an
+// `empty` mbarrier per stage: warp 0 waits for the slowest warp); REFILL 1: the
+// last warp to finish with a stage refills it at once (a shared counter).
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_, int GM_, int REFILL_ = 0>
 struct TmaCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
-  static constexpr int GM = GM_, BK = 16;
+  static constexpr int GM = GM_, BK = 16, REFILL = REFILL_;
   static constexpr int WARPS = (BM / WM) * (BN / WN), THREADS = 32 * WARPS;
   static constexpr int MI = WM / 16, NI = WN / 8;
   static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 16 * STAGES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 20 * STAGES;
   static_assert(WM % 16 == 0 && WN % 16 == 0 && BM % WM == 0 && BN % WN == 0, "tile shape");
   static_assert(BM <= 256, "one TMA box of A per slab");
 };
 // 4 warps of 32x32, three CTAs per SM: 96.9% of the DMMA peak at c4 and 94.9%
-// at c3 (vs 93.4% / 92.6% for 64x128 with 8 warps), profiles/r01_tune_dmma_tma_cfgs.jsonl
-using TmaMain = TmaCfg<64, 64, 32, 32, 4, 3, 8>;
+// at c3 (vs 93.4% / 92.6% for 64x128 with 8 warps), profiles/r01_tune_dmma_tma_cfgs.jsonl;
+// last-warp refill: c4 246.2 -> 243.6 ms (97.7%), c3 unchanged, bit-identical
+// (profiles/r02_tune_dmma_refill.jsonl)
+using TmaMain = TmaCfg<64, 64, 32, 32, 4, 3, 8, 1>;
 
 using tma::load_2d;
 using tma::mbar_arrive;
@@ -87,6 +92,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   unsigned char* base = tma::align1k(tm_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + Cfg::STAGES;  // one arrival per warp when it is done with a slab
+  unsigned* done_warps = reinterpret_cast<unsigned*>(empty + Cfg::STAGES);  // REFILL 1
 
   const int64_t pid = blockIdx.x;
   const int64_t width = Cfg::GM * tiles_n;
@@ -104,6 +110,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     for (int s = 0; s < Cfg::STAGES; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::WARPS);
+      done_warps[s] = 0;
     }
     tma::mbar_init_fence();
   }
@@ -177,12 +184,30 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 #pragma unroll
         for (int ni = 0; ni < Cfg::NI; ni++) dmma_step(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
     }
-    tma::release_stage(&empty[stage], lane);
-    // refill the slab of iteration kt-1 with k-slab kt-1+STAGES
-    if (tid == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
-      const int ps = (int)((kt - 1) % Cfg::STAGES);
-      mbar_wait(&empty[ps], (unsigned)(((kt - 1) / Cfg::STAGES) & 1));
-      issue(ps, kt - 1 + Cfg::STAGES);
+    if constexpr (Cfg::REFILL == 1) {
+      // count this warp out of the stage (its reads ordered before the async
+      // proxy's refill); the last warp out refills it with slab kt + STAGES
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        unsigned before;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(before)
+                     : "r"(tma::smem_addr(&done_warps[stage]))
+                     : "memory");
+        if (before == Cfg::WARPS - 1) {
+          done_warps[stage] = 0;  // before the refill's expect_tx arrive (a release)
+          if (kt + Cfg::STAGES < KT) issue(stage, kt + Cfg::STAGES);
+        }
+      }
+    } else {
+      tma::release_stage(&empty[stage], lane);
+      // refill the slab of iteration kt-1 with k-slab kt-1+STAGES
+      if (tid == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
+        const int ps = (int)((kt - 1) % Cfg::STAGES);
+        mbar_wait(&empty[ps], (unsigned)(((kt - 1) / Cfg::STAGES) & 1));
+        issue(ps, kt - 1 + Cfg::STAGES);
+      }
     }
   }
 

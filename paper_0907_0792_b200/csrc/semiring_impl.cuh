@@ -491,8 +491,8 @@ cudaError_t semiring_acc(const Problem& p) {
     return p.accumulate ? tropical_candidate<C, R, true>(p) : tropical_candidate<C, R, false>(p);
   } else if constexpr (i32trop) {
     if (tropical_tma_eligible(p))
-      return p.accumulate ? tropical_tma_launch<C, R, 3, true, 3, 1, true, 64>(p, nullptr)
-                          : tropical_tma_launch<C, R, 3, false, 3, 1, true, 64>(p, nullptr);
+      return p.accumulate ? tropical_tma_launch<C, R, 3, true, 3, 1, true, 64, 1>(p, nullptr)
+                          : tropical_tma_launch<C, R, 3, false, 3, 1, true, 64, 1>(p, nullptr);
     return p.accumulate ? semiring_launch<T, C, R, true, -1>(p, nullptr)
                         : semiring_launch<T, C, R, false, -1>(p, nullptr);
   } else {

@@ -281,8 +281,13 @@ constexpr int TT_A_BYTES = TropTma<128>::A_BYTES, TT_B_BYTES = TropTma<128>::B_B
 constexpr int TT_STAGE_BYTES = TropTma<128>::STAGE_BYTES;
 constexpr size_t TT_SMEM = TropTma<128>::SMEM;
 
+// REFILL 0: thread 0 refills the slab consumed one iteration earlier once
+// every warp has released it (empty mbarrier), i.e. warp 0 waits for the
+// slowest warp each k-slab; REFILL 1: the LAST warp to finish a slab refills
+// its stage at once (a shared counter per stage), so no warp ever waits on
+// another's progress except for data.
 template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false,
-          int BMT = 128>
+          int BMT = 128, int REFILL = 0>
 __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
     tropical_tma_kernel(float* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                         const unsigned* special, int64_t tiles_m, int64_t tiles_n,
@@ -299,6 +304,7 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
   unsigned char* base = tma::align1k(tt_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + TSTAGES * TT::STAGE_BYTES);
   uint64_t* empty = full + TSTAGES;
+  unsigned* done_warps = reinterpret_cast<unsigned*>(empty + TSTAGES);  // REFILL 1
 
   const int64_t pid = blockIdx.x;
   constexpr int GM = 8;
@@ -314,13 +320,14 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
     for (int s = 0; s < TSTAGES; s++) {
       tma::mbar_init(&full[s], 1);
       tma::mbar_init(&empty[s], TT::THREADS / 32);
+      done_warps[s] = 0;
     }
     tma::mbar_init_fence();
   }
   __syncthreads();
 
   const int64_t KT = (K + TBK - 1) / TBK;
-  auto issue = [&](int stage, int64_t kt) {  // thread 0 only
+  auto issue = [&](int stage, int64_t kt) {  // one thread
     unsigned char* st = base + stage * TT::STAGE_BYTES;
     tma::mbar_expect_tx(&full[stage], TT::STAGE_BYTES);
     tma::load_2d(st, &map_a, (int)(kt * TBK), (int)m0, &full[stage]);
@@ -430,12 +437,33 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
           }
       }
     }
-    tma::release_stage(&empty[stage], lane);
-    // refill the slab consumed one iteration ago (its readers are long done)
-    if (tid == 0 && kt >= 1 && kt - 1 + TSTAGES < KT) {
-      const int ps = (int)((kt - 1) % TSTAGES);
-      tma::mbar_wait(&empty[ps], (unsigned)(((kt - 1) / TSTAGES) & 1));
-      issue(ps, kt - 1 + TSTAGES);
+    if constexpr (REFILL == 1) {
+      // this warp's reads of the stage before the async proxy's refill, then
+      // count the warp out; the last one (acq_rel: every other warp's reads
+      // happen-before) refills the stage with slab kt + TSTAGES
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        unsigned before;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(before)
+                     : "r"(tma::smem_addr(&done_warps[stage]))
+                     : "memory");
+        if (before == TT::THREADS / 32 - 1) {
+          // reset before the refill's expect_tx arrive (a release), which the
+          // warps' next wait on this stage acquires
+          done_warps[stage] = 0;
+          if (kt + TSTAGES < KT) issue(stage, kt + TSTAGES);
+        }
+      }
+    } else {
+      tma::release_stage(&empty[stage], lane);
+      // refill the slab consumed one iteration ago (its readers are long done)
+      if (tid == 0 && kt >= 1 && kt - 1 + TSTAGES < KT) {
+        const int ps = (int)((kt - 1) % TSTAGES);
+        tma::mbar_wait(&empty[ps], (unsigned)(((kt - 1) / TSTAGES) & 1));
+        issue(ps, kt - 1 + TSTAGES);
+      }
     }
   }
 
@@ -468,14 +496,14 @@ inline bool tropical_tma_eligible(const Problem& p) {
 }
 
 template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false,
-          int BMT = 128>
+          int BMT = 128, int REFILL = 0>
 cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
   using TT = TropTma<BMT>;
   CUtensorMap map_a, map_b;
   if (!make_tensor_map_2d(&map_a, p.a, 4, p.M, p.K, p.lda, TT::BM, TBK, true) ||
       !make_tensor_map_2d(&map_b, p.b, 4, p.K, p.N, p.ldb, TBK, TBN, false))
     return cudaErrorInvalidValue;
-  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR, QUAD, BMT>;
+  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR, QUAD, BMT, REFILL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + TT::BM - 1) / TT::BM, tiles_n = (p.N + TBN - 1) / TBN;
@@ -497,7 +525,9 @@ cudaError_t tropical_launch(const Problem& p, const unsigned* special) {
   // 128 registers) and 228.7 ms for those with the two-k step; 1000^3
   // 0.089 vs 0.146 ms (twice the CTAs) — profiles/r01_tune_tropical_quad.jsonl,
   // r01_tune_tropical_bm64.jsonl
-  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE, ACC, 3, 1, true, 64>(p, special);
+  // Each stage is refilled by the last warp to release it (REFILL 1: c5 218.3
+  // -> 211.2 ms, bit-identical, profiles/r02_tune_tropical_refill.jsonl).
+  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE, ACC, 3, 1, true, 64, 1>(p, special);
   const bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);
