@@ -411,14 +411,17 @@ def measure_e2e(w, rows_range, a_pin, b_pin, steps, warmup, device, world, rank,
             return fn(A, B, w.ops)
     else:
         gplan = job_plan(w, world)
-        a_blk = a_pin[r0 * plan.lstride:r1 * plan.lstride] if SCALING[w.key] == "strong" \
-            else a_pin  # weak scaling: this rank's unit is its whole A
+        # strong scaling: this rank's rows of A (a_pin may already be just the
+        # block); weak scaling: this rank's unit is its whole A
+        nblk = (r1 - r0) * plan.lstride
+        a_blk = a_pin[r0 * plan.lstride:r1 * plan.lstride] \
+            if SCALING[w.key] == "strong" and a_pin.numel() != nblk else a_pin
 
         def step():
             return sharded_product_host(gplan, a_blk, b_pin if rank == 0 else None, w.ops,
                                         device=device, group=group)
-    # results are returned in pinned host memory from torch's caching host
-    # allocator; drop each step's result before the next so the cache reuses it
+    # results come back in the library's page-locked host blocks; drop each
+    # step's result before the next so its block is reused
     out = None
     for _ in range(warmup):
         out = None
@@ -623,7 +626,11 @@ def inner_leg(key, device, world, rank, group=None) -> dict:
            "rows_per_rank": rr[1] - rr[0], "kernel_ms": round(kern_ms, 4),
            "roofline": roofline(wi, rr[1] - rr[0], kern_ms, d["clocks"].get("sm_mhz")),
            "clocks": d["clocks"], "gpu_launches": d["launches"]}
-    ap, bp = pinned_copy(ai), pinned_copy(bi)
+    if world == 1:
+        ap, bp = pinned_copy(ai), pinned_copy(bi)
+    else:  # each rank pins only what it sends: its A rows, and B on rank 0
+        ap = pinned_copy(ai[rr[0] * ki:rr[1] * ki])
+        bp = pinned_copy(bi) if rank == 0 else None
     e2e_st = 20 if key == "c1" else 3
     el_i = measure_e2e(wi, rr, ap, bp, e2e_st, 3, device, world, rank, group)
     if world == 1:

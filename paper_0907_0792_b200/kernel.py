@@ -154,8 +154,15 @@ def result_dtype(a: MoaArray, b: MoaArray) -> np.dtype:
     return _F64
 
 
+_NP_CODES = {_F64: _native.DTYPE_F64, _F32: _native.DTYPE_F32, _I32: _native.DTYPE_I32,
+             _I64: _native.DTYPE_I64}
+
+
 def native_dtype(dt) -> int:
     """ABI dtype code for a numpy or torch dtype."""
+    code = _NP_CODES.get(dt) if isinstance(dt, np.dtype) else None
+    if code is not None:
+        return code
     name = str(dt).replace("torch.", "")
     return {"float64": _native.DTYPE_F64, "float32": _native.DTYPE_F32,
             "int32": _native.DTYPE_I32, "int64": _native.DTYPE_I64}[name]
