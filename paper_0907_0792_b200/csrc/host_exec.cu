@@ -157,6 +157,7 @@ struct Session {
     if (err == cudaSuccess && e != cudaSuccess) err = e;
   }
   ~Session() {
+    const auto t0 = std::chrono::steady_clock::now();
     if (q) {
       if (err != cudaSuccess || !pooled.empty()) {
         // drain every queue before buffers or the queue set are reused
@@ -168,6 +169,9 @@ struct Session {
       moa::host::checkin(q);
     }
     if (prev_device >= 0 && prev_device != device) cudaSetDevice(prev_device);
+    if (std::getenv("MOA_HOST_TRACE"))
+      fprintf(stderr, "[moa_host] cleanup=%.3f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
 };
 

@@ -51,7 +51,7 @@ Queues* checkout(int device, cudaError_t& err);
 void checkin(Queues* q);
 
 // Private stream-ordered pool of `device` (release threshold
-// $MOA_HOST_POOL_KEEP_BYTES, default 4 GiB).
+// $MOA_HOST_POOL_KEEP_BYTES, default 16 GiB).
 cudaMemPool_t device_pool(int device, cudaError_t& err);
 
 // Is host memory at p page-locked (pinned or registered with CUDA)?

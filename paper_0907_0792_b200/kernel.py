@@ -356,6 +356,7 @@ def execute_sequential(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair =
 
 
 _HUGE_PAGE = 2 << 20
+_TRACE = bool(__import__("os").environ.get("MOA_HOST_TRACE"))
 
 
 def host_empty(n: int, dtype) -> np.ndarray:
@@ -390,12 +391,23 @@ def execute_host(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair = MUL_A
     large products stream in row blocks with the copies overlapping the
     kernels (B in k-chunks behind the first block).  The result is ordinary
     pageable memory (``host_empty``)."""
+    import time as _time
+    t0 = _time.perf_counter()
     torch = _torch()
     _native.load()
     dtype = result_dtype(a, b)
     host_a = np.ascontiguousarray(a.data if a.data.dtype == dtype else a.data.astype(dtype)).ravel()
     host_b = np.ascontiguousarray(b.data if b.data.dtype == dtype else b.data.astype(dtype)).ravel()
+    t1 = _time.perf_counter()
     out = host_empty(plan.noproc * plan.elsinop, dtype)
+    t2 = _time.perf_counter()
     dev = torch.cuda.current_device() if device is None else torch.device(device).index
     launch_host(plan, out, host_a, host_b, ops, exact=exact, device=dev)
-    return MoaArray._wrap(plan.result_shape, out)
+    t3 = _time.perf_counter()
+    res = MoaArray._wrap(plan.result_shape, out)
+    if _TRACE:
+        import sys as _sys
+        print(f"[execute_host] operands={1e3 * (t1 - t0):.3f} alloc={1e3 * (t2 - t1):.3f} "
+              f"call={1e3 * (t3 - t2):.3f} wrap={1e3 * (_time.perf_counter() - t3):.3f} ms",
+              file=_sys.stderr)
+    return res
