@@ -631,16 +631,17 @@ def inner_leg(key, device, world, rank, group=None) -> dict:
     else:  # each rank pins only what it sends: its A rows, and B on rank 0
         ap = pinned_copy(ai[rr[0] * ki:rr[1] * ki])
         bp = pinned_copy(bi) if rank == 0 else None
-    e2e_st = 20 if key == "c1" else 3
+    e2e_st = 20 if key == "c1" else 5
     el_i = measure_e2e(wi, rr, ap, bp, e2e_st, 3, device, world, rank, group)
     if world == 1:
-        el_c = measure_e2e_cabi(wi, ap, bp, e2e_st, 3, device)
+        with ClockSampler(device.index) as e2e_clocks:
+            el_c = measure_e2e_cabi(wi, ap, bp, e2e_st, 3, device)
         leg["e2e"] = {"value": round(to_unit(wi, amt * e2e_st, el_c), 2), "unit": METRIC[key][1],
                       "ms_per_step": round(el_c / e2e_st * 1e3, 3),
                       "h2d_bytes_per_step": (mi * ki + ki * ni) * isz,
                       "d2h_bytes_per_step": mi * ni * isz,
                       "path": "moa_product_rows_host (C ABI) on page-locked host buffers "
-                              "(streamed row blocks)"}
+                              "(streamed row blocks)", "clocks": e2e_clocks.summary()}
         leg["e2e_api"] = {"value": round(to_unit(wi, amt * e2e_st, el_i), 2),
                           "unit": METRIC[key][1], "ms_per_step": round(el_i / e2e_st * 1e3, 3),
                           "path": "moa.inner on pinned host MoaArrays (streamed row blocks)"}
