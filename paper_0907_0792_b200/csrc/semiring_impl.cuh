@@ -32,6 +32,7 @@
 
 #include <type_traits>
 
+#include "host_runtime.h"
 #include "moa_common.cuh"
 #include "moa_kernels.h"
 #include "../../include/moa_b200.h"
@@ -458,10 +459,23 @@ namespace {
 // unsigned-order fold): pre-scan A (M x K, lda), B (K x N, ldb) and, when
 // accumulating, C (M x N, ldc) for NaN / +-inf / +-0 / sign, then launch one
 // specialisation per fold mode; all but the one the flags select exit at once.
+//
+// The 12-byte flags buffer comes from the library's private device pool
+// (host_runtime.cu), which keeps its memory mapped: from the device's default
+// pool (release threshold 0) every launch re-mapped a fresh chunk after the
+// previous one had been unmapped at a synchronisation, and those mapping
+// operations intermittently blocked the host for tens of ms while kernels
+// were in flight — the k-chunked accumulate schedule of c5's first block took
+// 42-136 ms from one repetition to the next (tools/c5_repeat_device.py).
 template <int C, int R, bool ACC>
 cudaError_t tropical_candidate(const Problem& p) {
   unsigned* special = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&special), 3 * sizeof(unsigned), p.stream);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  cudaMemPool_t pool = e == cudaSuccess ? host::device_pool(dev, e) : nullptr;
+  if (pool == nullptr) return e != cudaSuccess ? e : cudaErrorMemoryAllocation;
+  e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&special), 3 * sizeof(unsigned), pool,
+                              p.stream);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(special, 0, 3 * sizeof(unsigned), p.stream);
   if (e == cudaSuccess) {

@@ -3,7 +3,7 @@
 // and checked bit for bit against the production variant.  Prints JSON lines.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
 //   -I paper_0907_0792_b200/csrc -I include -o tools/tune_tropical tools/tune_tropical.cu \
-//   paper_0907_0792_b200/csrc/tma.cu
+//   paper_0907_0792_b200/csrc/tma.cu paper_0907_0792_b200/csrc/host_runtime.cu
 // Usage: tools/tune_tropical [N=16384] [reps=3]
 #include <cstdio>
 #include <cstdlib>
