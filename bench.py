@@ -105,11 +105,14 @@ def theoretical(key: str, sm_mhz: float | None) -> dict:
     """The pipe's nominal ceiling at the run's SM clock (max clock if unsampled)."""
     mhz = sm_mhz or 1965.0
     if key == "c5":
-        # one FADD2 + one 3-input min per two pairs: 1 warp-instruction per
-        # 32 pairs, 4 issue slots per SM per clock
-        return {"value": round(SM_COUNT * 4 * 32 * mhz * 1e6 / 1e9, 1), "unit": "Gpairs/s",
-                "what": "issue limit: 1 instruction per pair per lane (FADD2 + 3-input min "
-                        "per 2 pairs), 4 schedulers x 32 lanes x 148 SMs", "sm_mhz": mhz}
+        # one FADD2 + one VIMNMX3 per 64 pairs of a warp; FADD2 holds the
+        # issue port two clocks (0.49/clk alone, FADD 0.95/clk, FADD+VIMNMX3
+        # 0.97/clk: profiles/r02_mb_dualissue.json), so 3 issue clocks per 64
+        # pairs on each of 4 schedulers (profiles/r02_c5_ceiling.md)
+        return {"value": round(SM_COUNT * 4 * 64 / 3 * mhz * 1e6 / 1e9, 1), "unit": "Gpairs/s",
+                "what": "issue limit: FADD2 (2 issue clocks) + VIMNMX3 (1) per 64 pairs per warp, "
+                        "4 schedulers x 148 SMs (one-clock FADD2 would give 1.5x this)",
+                "sm_mhz": mhz}
     if key == "c2":
         return {"value": None, "unit": "GB/s", "what": "write-only ceiling measured: cudaMemset "
                 f"{microbench_peaks().get('memset_GBs')} GB/s (profiles/r01_peaks_microbench.json)"}

@@ -497,13 +497,18 @@ cudaError_t semiring_acc(const Problem& p) {
   constexpr bool cand = std::is_same<T, float>::value && (C == C_ADD || C == C_SUB || C == C_MUL) &&
                         (R == R_MIN || R == R_MAX);
   // int32 (add|subtract, min|max): exact integer arithmetic, so the TMA
-  // tropical kernel (64x128 tiles, four-k step) runs it with one DPX
+  // tropical kernel (four-k step; 128x128 tiles from 256 of them, 64x128
+  // below, as for float32: 250.4 vs 250.9 ms at 16384^3, 0.157 vs 0.099 ms at
+  // 1000^3, profiles/r02_tune_tropical_bm128.jsonl) runs it with one DPX
   // VIADDMNMX per pair and no pre-scan whenever rows are 16-byte aligned
   constexpr bool i32trop = std::is_same<T, int32_t>::value && (C == C_ADD || C == C_SUB) &&
                            (R == R_MIN || R == R_MAX);
   if constexpr (cand) {
     return p.accumulate ? tropical_candidate<C, R, true>(p) : tropical_candidate<C, R, false>(p);
   } else if constexpr (i32trop) {
+    if (tropical_tma_eligible(p) && tropical_big_tiles(p))
+      return p.accumulate ? tropical_tma_launch<C, R, 3, true, 2, 1, true, 128, 1>(p, nullptr)
+                          : tropical_tma_launch<C, R, 3, false, 2, 1, true, 128, 1>(p, nullptr);
     if (tropical_tma_eligible(p))
       return p.accumulate ? tropical_tma_launch<C, R, 3, true, 3, 1, true, 64, 1>(p, nullptr)
                           : tropical_tma_launch<C, R, 3, false, 3, 1, true, 64, 1>(p, nullptr);

@@ -3,8 +3,9 @@
 // only), reduce in {min, max} — in their own kernels.
 //
 // Two kernels share the loop: tropical_tma_kernel (16-byte aligned rows:
-// TMA-staged tiles, mbarrier pipeline, no block barrier in the main loop; 64x128
-// C tiles of 128 threads, three CTAs per SM, four k per step) and
+// TMA-staged tiles, mbarrier pipeline, no block barrier in the main loop;
+// 128x128 C tiles of 256 threads, two CTAs per SM, for large outputs and 64x128
+// tiles of 128 threads, three CTAs per SM, below that; four k per step) and
 // tropical_kernel (any alignment: cp.async into padded A[BM][BK+4],
 // B[BK][BN+4]; 128x128 tiles).  Operands stay in their natural row-major
 // layouts; a thread owns 8 rows and columns 64g + 4tx + c (g < 2, c < 4) of
@@ -281,13 +282,18 @@ constexpr int TT_A_BYTES = TropTma<128>::A_BYTES, TT_B_BYTES = TropTma<128>::B_B
 constexpr int TT_STAGE_BYTES = TropTma<128>::STAGE_BYTES;
 constexpr size_t TT_SMEM = TropTma<128>::SMEM;
 
+// FORM (the FADD2/fold pairing; all bit-identical): 0 = row k's and row k+1's
+// column pairs folded lo with lo, hi with hi (production); 1 = row k+1's pair
+// swapped inside its FADD2 (.LO_HI operand) so each fold reads one even and
+// one odd register; 2 = scalar FADDs.  1 and 2 measured slower at c5 (213.6
+// and 246.3 vs 211.2 ms, profiles/r02_tune_tropical_form.jsonl).
 // REFILL 0: thread 0 refills the slab consumed one iteration earlier once
 // every warp has released it (empty mbarrier), i.e. warp 0 waits for the
 // slowest warp each k-slab; REFILL 1: the LAST warp to finish a slab refills
 // its stage at once (a shared counter per stage), so no warp ever waits on
 // another's progress except for data.
 template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false,
-          int BMT = 128, int REFILL = 0>
+          int BMT = 128, int REFILL = 0, int FORM = 0>
 __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
     tropical_tma_kernel(float* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                         const unsigned* special, int64_t tiles_m, int64_t tiles_n,
@@ -362,6 +368,17 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
           if constexpr (I32) {  // k then k+1, as the exact loop folds them
             acc[i][j] = iaddmnmx<C, R>(a1, y0, iaddmnmx<C, R>(a0, x0, acc[i][j]));
             acc[i][j + 1] = iaddmnmx<C, R>(a1, y1, iaddmnmx<C, R>(a0, x1, acc[i][j + 1]));
+          } else if constexpr (FORM == 2) {
+            // scalar adds (FADD: one issue slot per pair, as FADD2 costs two)
+            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], CombineOp<C>::f(a0, x0), CombineOp<C>::f(a1, y0));
+            acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], CombineOp<C>::f(a0, x1), CombineOp<C>::f(a1, y1));
+          } else if constexpr (FORM == 1) {
+            // row k+1's pair enters its FADD2 swapped (free: the .LO_HI operand
+            // form), so each 3-input fold reads one even and one odd register
+            const unsigned long long s = pair_op_bcast<C>(x0, x1, a0);
+            const unsigned long long t = pair_op_bcast<C>(y1, y0, a1);
+            acc[i][j] = fold3<R, INTFOLD>(acc[i][j], lo32(s), hi32(t));
+            acc[i][j + 1] = fold3<R, INTFOLD>(acc[i][j + 1], hi32(s), lo32(t));
           } else {
             const unsigned long long s = pair_op_bcast<C>(x0, x1, a0);
             const unsigned long long t = pair_op_bcast<C>(y0, y1, a1);
@@ -496,14 +513,14 @@ inline bool tropical_tma_eligible(const Problem& p) {
 }
 
 template <int C, int R, int MODE, bool ACC, int MINB = 2, int UNR = 1, bool QUAD = false,
-          int BMT = 128, int REFILL = 0>
+          int BMT = 128, int REFILL = 0, int FORM = 0>
 cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
   using TT = TropTma<BMT>;
   CUtensorMap map_a, map_b;
   if (!make_tensor_map_2d(&map_a, p.a, 4, p.M, p.K, p.lda, TT::BM, TBK, true) ||
       !make_tensor_map_2d(&map_b, p.b, 4, p.K, p.N, p.ldb, TBK, TBN, false))
     return cudaErrorInvalidValue;
-  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR, QUAD, BMT, REFILL>;
+  auto kern = tropical_tma_kernel<C, R, MODE, ACC, MINB, UNR, QUAD, BMT, REFILL, FORM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TT::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + TT::BM - 1) / TT::BM, tiles_n = (p.N + TBN - 1) / TBN;
@@ -513,6 +530,11 @@ cudaError_t tropical_tma_launch(const Problem& p, const unsigned* special) {
       static_cast<float*>(p.c), p.M, p.N, p.K, p.ldc, special, tiles_m, tiles_n, map_a, map_b);
   count_launch();
   return cudaGetLastError();
+}
+
+// 128 x 128 CTA tiles once there are >= 256 of them (see tropical_launch)
+inline bool tropical_big_tiles(const Problem& p) {
+  return ((p.M + 127) / 128) * ((p.N + 127) / 128) >= 256;
 }
 
 template <int C, int R, int MODE, bool ACC>
@@ -527,7 +549,14 @@ cudaError_t tropical_launch(const Problem& p, const unsigned* special) {
   // r01_tune_tropical_bm64.jsonl
   // Each stage is refilled by the last warp to release it (REFILL 1: c5 218.3
   // -> 211.2 ms, bit-identical, profiles/r02_tune_tropical_refill.jsonl).
-  if (tropical_tma_eligible(p)) return tropical_tma_launch<C, R, MODE, ACC, 3, 1, true, 64, 1>(p, special);
+  // With the last-warp refill, 128 x 128 tiles of 256 threads (two CTAs and
+  // 16 warps per SM at 128 registers) overtake the 64 x 128 ones from 256 such
+  // tiles up: c5 206.7 vs 211.2 ms, 2048^3 0.484 vs 0.516 ms, 1000^3 0.136 vs
+  // 0.083 ms (profiles/r02_tune_tropical_bm128.jsonl).
+  if (tropical_tma_eligible(p)) {
+    if (tropical_big_tiles(p)) return tropical_tma_launch<C, R, MODE, ACC, 2, 1, true, 128, 1>(p, special);
+    return tropical_tma_launch<C, R, MODE, ACC, 3, 1, true, 64, 1>(p, special);
+  }
   const bool vec = (p.lda % 4 == 0) && (p.ldb % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.a) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(p.b) % 16 == 0);

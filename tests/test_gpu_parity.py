@@ -657,7 +657,9 @@ def test_row_sets_equal_full_launch_every_route(mkn, rng):
                               f"{np.dtype(dt).name} {ops} rows {r0}:{r1}")
 
 
-@pytest.mark.parametrize("mkn", [(300, 132, 260), (257, 131, 300)])  # TMA / cp.async kernels
+@pytest.mark.parametrize("mkn", [(300, 132, 260),    # TMA kernel, 64x128 tiles
+                                 (257, 131, 300),    # cp.async kernel
+                                 (2049, 37, 2052)])  # TMA kernel, >= 256 128x128 tiles, ragged
 def test_tropical_accumulate_seeds(mkn, rng):
     """float32 (add|subtract|multiply, min|max) under MOA_FLAG_ACCUMULATE with
     the reference's identity prefill (+-inf), with negative and with mixed
@@ -798,13 +800,13 @@ def test_tropical_tma_strided_rows_odd_k(rng):
             assert not np.delete(got, np.s_[0::step], axis=0).any()
 
 
-@pytest.mark.parametrize("k", [70, 67])
-def test_tropical_quad_step_on_full_grids(k, rng):
-    """Grids of >= 296 128x128 tiles take the four-k step of the TMA tropical
-    kernel (tail: one k-pair and/or a lone k); every fast fold mode — unsigned
-    order (VIMNMX3), signed (FMNMX3), max-times (FMUL2) — bitwise vs the
-    reference and vs the exact loop."""
-    m, n = 2048, 2432
+@pytest.mark.parametrize("k,m,n", [(70, 2048, 2432), (67, 2048, 2432), (67, 2049, 2436)])
+def test_tropical_quad_step_on_full_grids(k, m, n, rng):
+    """Grids of >= 256 128x128 tiles run the TMA tropical kernel's 128x128
+    tiles (256 threads, four-k step; tail: one k-pair and/or a lone k; ragged
+    last row and column tiles); every fast fold mode — unsigned order
+    (VIMNMX3), signed (FMNMX3), max-times (FMUL2) — bitwise vs the reference
+    and vs the exact loop."""
     cases = (("add", "min", 0.0), ("subtract", "max", 50.0), ("multiply", "max", 0.0))
     for comb, red, shift in cases:
         ops = op_pair(comb, red)
@@ -1083,14 +1085,15 @@ def test_integer_tropical_wraps(rng):
             np.testing.assert_array_equal(got, want, err_msg=f"{np.dtype(dt).name} {comb}/{red}")
 
 
-@pytest.mark.parametrize("k,lstride", [(68, 68), (67, 68), (130, 132)])
-def test_int32_tropical_tma_route_wraps(k, lstride, rng):
+@pytest.mark.parametrize("k,lstride,m,n", [(68, 68, 300, 260), (67, 68, 300, 260),
+                                           (130, 132, 300, 260), (13, 16, 2049, 2052)])
+def test_int32_tropical_tma_route_wraps(k, lstride, m, n, rng):
     """int32 (add|subtract, min|max) with 16-byte aligned rows runs the TMA
     tropical kernel (one VIADDMNMX per pair, four-k step, pair and lone-k
-    tails when K is odd): full-range values, two's-complement wrap before the
-    fold, write-only and accumulate, bitwise vs numpy."""
+    tails when K is odd; 64x128 tiles, and 128x128 ones from 256 of them):
+    full-range values, two's-complement wrap before the fold, write-only and
+    accumulate, bitwise vs numpy."""
     torch = _torch()
-    m, n = 300, 260
     info = np.iinfo(np.int32)
     a = rng.integers(info.min, info.max, size=(m, lstride), endpoint=True, dtype=np.int64).astype(np.int32)
     b = rng.integers(info.min, info.max, size=(k, n), endpoint=True, dtype=np.int64).astype(np.int32)

@@ -4,7 +4,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
 //   -I paper_0907_0792_b200/csrc -I include -o tools/tune_tropical tools/tune_tropical.cu \
 //   paper_0907_0792_b200/csrc/tma.cu paper_0907_0792_b200/csrc/host_runtime.cu
-// Usage: tools/tune_tropical [N=16384] [reps=3]
+// Usage: tools/tune_tropical [N=16384] [reps=3] [which=0: all variants, 1: bm128 only, 2: int32 DPX bm64 vs bm128]
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -90,12 +90,30 @@ int main(int argc, char** argv) {
            name, (long long)n, ms, pairs / ms / 1e6, (long long)diffs);
     fflush(stdout);
   };
+  if (argc > 3 && atoi(argv[3]) == 2) {  // int32 (add, min) on the DPX route: bm64 vs bm128
+    p.dtype = 2;
+    p.c = c0;
+    report("int32_bm64_quad_refill1", c0, time_ms([&] { return tropical_tma_launch<C_ADD, R_MIN, 3, false, 3, 1, true, 64, 1>(p, nullptr); }, reps));
+    p.c = c1;
+    CK(cudaMemset(c1, 0, n * n * 4));
+    report("int32_bm128_quad_refill1", c1, time_ms([&] { return tropical_tma_launch<C_ADD, R_MIN, 3, false, 2, 1, true, 128, 1>(p, nullptr); }, reps));
+    return 0;
+  }
   p.c = c0;
-  double ms = time_ms([&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 3, 1, true, 64, 0>(p, special); }, reps);
-  report("production_bm64_quad_refill0", c0, ms);
+  double ms = time_ms([&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 3, 1, true, 64, 1>(p, special); }, reps);
+  report("production_bm64_quad_refill1", c0, ms);
   p.c = c1;
-  CK(cudaMemset(c1, 0, n * n * 4));
-  ms = time_ms([&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 3, 1, true, 64, 1>(p, special); }, reps);
-  report("bm64_quad_refill1_last_warp", c1, ms);
+  auto variant = [&](const char* name, auto launch) {
+    CK(cudaMemset(c1, 0, n * n * 4));
+    report(name, c1, time_ms(launch, reps));
+  };
+  const int which = argc > 3 ? atoi(argv[3]) : 0;
+  if (which == 0 || which == 1)
+    variant("bm128_quad_refill1", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 2, 1, true, 128, 1, 0>(p, special); });
+  if (which == 0) {
+    variant("bm64_quad_refill1_form1_swapped", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 3, 1, true, 64, 1, 1>(p, special); });
+    variant("bm64_quad_refill1_form2_scalar_fadd", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 3, 1, true, 64, 1, 2>(p, special); });
+    variant("bm128_quad_refill1_form1_swapped", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 2, 1, true, 128, 1, 1>(p, special); });
+  }
   return 0;
 }
