@@ -114,6 +114,22 @@ std::vector<std::pair<int64_t, int64_t>> k_chunks(int64_t K, int chunks, int64_t
   return out;
 }
 
+// Write-only single-block products with a page-locked res up to this many
+// result bytes ($MOA_HOST_DIRECT_OUT_BYTES overrides it; 0 disables) store
+// their rows straight into res through its device mapping: no device result
+// buffer and no D2H copy after the kernel, whose start trails the kernel by
+// ~8 us.  The kernels' stores reach ~28 GB/s over PCIe against the copy
+// engine's ~55, so this pays only for small results: c1 (512 KiB) 62.4 vs
+// 65.7 us per call, 1024^3 f64 (8 MiB) 756 vs 560 us
+// (profiles/r02_c1_e2e_probe.log).
+size_t direct_out_bytes() {
+  static const size_t v = [] {
+    if (const char* e = std::getenv("MOA_HOST_DIRECT_OUT_BYTES")) return (size_t)std::strtoull(e, nullptr, 10);
+    return (size_t)1 << 20;
+  }();
+  return v;
+}
+
 // $MOA_HOST_TRACE=1: one stderr line per call with the host-side phase times
 struct Trace {
   const bool on = std::getenv("MOA_HOST_TRACE") != nullptr;
@@ -288,16 +304,29 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
                               (size_t)b_span * esz, 1, b_pin, st));
   };
 
-  // ---- one block: everything in order on one queue, no events
+  // ---- one block: in order on one queue (page-locked B copies in on a
+  // second queue, concurrently with A; a small write-only result goes
+  // straight into page-locked res)
   if (blocks.size() == 1) {
     cudaStream_t st = q.s_comp;
+    const size_t out_bytes = (size_t)(rows * N) * esz;
+    const bool split_in = K > 0 && a_pin && b_pin;
+    cudaStream_t sb = split_in ? q.s_in : st;
+    char* c_direct = (!acc && r_pin && out_bytes <= direct_out_bytes())
+                         ? static_cast<char*>(moa::host::device_view(c_rows))
+                         : nullptr;
     char* a_dev = static_cast<char*>(ss.alloc(0, (size_t)(K > 0 ? a_span : 0) * esz, st));
-    char* b_dev = static_cast<char*>(ss.alloc(1, (size_t)(K > 0 ? b_span : 0) * esz, st));
-    char* c_dev = static_cast<char*>(ss.alloc(2, (size_t)(rows * N) * esz, st));
+    char* b_dev = static_cast<char*>(ss.alloc(1, (size_t)(K > 0 ? b_span : 0) * esz, sb));
+    char* c_dev = c_direct ? c_direct : static_cast<char*>(ss.alloc(2, out_bytes, st));
     if (ss.err != cudaSuccess) return fail_cuda(ss.err, "device buffers");
     if (K > 0) {
       copy_a(a_dev, 0, rows, 0, K, st);
-      copy_b(b_dev, 0, K, st);
+      copy_b(b_dev, 0, K, sb);
+      if (split_in) {
+        cudaEvent_t b_in = ss.event();
+        ss.check(cudaEventRecord(b_in, sb));
+        ss.check(cudaStreamWaitEvent(st, b_in, 0));
+      }
     }
     if (acc)
       ss.check(moa::host::h2d(device, c_dev, (size_t)N * esz, c_rows, c_pitch, (size_t)N * esz,
@@ -305,15 +334,18 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product (copy in)");
     tr.mark("in");
     const int rc = moa_product_rows(dtype, c_dev, K > 0 ? a_dev : nullptr, K > 0 ? b_dev : nullptr,
-                                    rows, K, N, K > 0 ? lda : 0, K > 0 ? ldb : N, N, combine_code,
-                                    reduce_code, 0, 1, flags, st);
+                                    rows, K, N, K > 0 ? lda : 0, K > 0 ? ldb : N,
+                                    c_direct ? restride * step : N, combine_code, reduce_code, 0, 1,
+                                    flags, st);
     if (rc != 0) {
       ss.err = cudaErrorUnknown;  // drain before the queues are reused; message already set
       return rc;
     }
     tr.mark("launched");
-    const size_t out_bytes = (size_t)(rows * N) * esz;
-    if (r_pin && rows >= 4 && out_bytes >= (64ull << 20)) {
+    if (c_direct) {
+      ss.check(cudaStreamSynchronize(st));
+      tr.mark("out_direct");
+    } else if (r_pin && rows >= 4 && out_bytes >= (64ull << 20)) {
       // a large result leaves over four copy queues, which draw a little
       // more of the host link than one (tools/e2e_probe.py: 54.8 -> 56.9 GB/s)
       cudaEvent_t done = ss.event();

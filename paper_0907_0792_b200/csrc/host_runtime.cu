@@ -377,6 +377,16 @@ bool is_pinned(const void* p) {
   return attr.type == cudaMemoryTypeHost;
 }
 
+void* device_view(void* p) {
+  if (p == nullptr) return nullptr;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return attr.type == cudaMemoryTypeHost ? attr.devicePointer : nullptr;
+}
+
 // ---------------------------------------------------------------- transfers
 cudaError_t h2d(int device, void* dst, size_t dpitch, const void* src, size_t hpitch,
                 size_t width, size_t rows, bool pinned, cudaStream_t st) {

@@ -57,6 +57,11 @@ cudaMemPool_t device_pool(int device, cudaError_t& err);
 // Is host memory at p page-locked (pinned or registered with CUDA)?
 bool is_pinned(const void* p);
 
+// The device address of page-locked host memory at p (its mapping into the
+// device's address space; the same address under unified addressing), or
+// nullptr when p is not page-locked or not mapped.
+void* device_view(void* p);
+
 // rows x width bytes, host (pitch hpitch) -> device (pitch dpitch), on `st`.
 // Page-locked host memory: one asynchronous 2-D copy.  Pageable: packed
 // through staging slots by the copy threads; returns once every chunk is

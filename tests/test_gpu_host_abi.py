@@ -218,6 +218,52 @@ def _pinned_like(x):
     return t
 
 
+@pytest.mark.parametrize("dt", DTYPES)
+def test_direct_out_into_page_locked_res(dt, rng):
+    """Write-only single-block products with a page-locked res (pinned, and
+    registered moa_host_alloc memory) of <= 1 MiB store their rows straight
+    into res through its device mapping: the bits of the device entry point,
+    only the row set's rows written, for inner (every kernel family) and
+    outer products."""
+    from paper_0907_0792_b200 import _native
+    m, k, n = 300, 132, 260   # f64 result 609 KiB   # 16-byte rows: TMA kernels; odd K below: cp.async ones
+    for kk in (k, 67):
+        a, b = _operands(rng, m * kk, dt), _operands(rng, kk * n, dt)
+        plan = plan_inner((m, kk), (kk, n))
+        pa, pb = _pinned_like(a), _pinned_like(b)
+        for ops in (moa.MUL_ADD, op_pair("add", "min"), op_pair("subtract", "max"),
+                    op_pair("divide", "add"), op_pair("max", "multiply")):
+            for start, step in ((0, 1), (3, 4)):
+                res0 = np.full(m * n, 5, dtype=dt)
+                want = _device_result(plan, res0, a, b, ops, start=start, step=step)
+                got = _pinned_like(res0)
+                launch_host(plan, got, pa, pb, ops, start=start, step=step)
+                assert_bits_equal(got, want, f"{dt.__name__} {ops} K={kk} {start}::{step}")
+    # registered (huge-page) host block as res
+    esz = np.dtype(dt).itemsize
+    ptr = _native.host_alloc(m * n * esz)
+    try:
+        import ctypes
+        buf = (ctypes.c_char * (m * n * esz)).from_address(ptr)
+        got = np.frombuffer(buf, dtype=dt)
+        got[:] = 0
+        a, b = _operands(rng, m * k, dt), _operands(rng, k * n, dt)
+        plan = plan_inner((m, k), (k, n))
+        want = _device_result(plan, np.zeros(m * n, dtype=dt), a, b, op_pair("add", "max"))
+        launch_host(plan, got, _pinned_like(a), _pinned_like(b), op_pair("add", "max"))
+        assert_bits_equal(got, want, f"{dt.__name__} registered res")
+        del got, buf
+    finally:
+        _native.host_free(ptr)
+    # outer product straight into pinned res
+    x, y = _operands(rng, 300, dt), _operands(rng, 400, dt)
+    plan = plan_outer((300,), (400,))
+    want = _device_result(plan, np.zeros(300 * 400, dtype=dt), x, y, op_pair("multiply", "add"))
+    got = _pinned_like(np.zeros(300 * 400, dtype=dt))
+    launch_host(plan, got, _pinned_like(x), _pinned_like(y), op_pair("multiply", "add"))
+    assert_bits_equal(got, want, f"{dt.__name__} outer")
+
+
 @pytest.mark.parametrize("acc", [False, True])
 def test_pageable_staging_equals_page_locked(acc, rng):
     """Pageable host buffers above the direct-copy size are staged through
