@@ -80,11 +80,17 @@ __device__ __forceinline__ int b_off(int k, int n) {
   return (n >> 4) * 2048 + k * 128 + (((((n & 15) >> 1) ^ k) & 7) << 4) + ((n & 1) << 3);
 }
 
-template <class Cfg, bool ACC>
+// PERSIST: gridDim.x <= tiles CTAs (one per resident slot), each taking tiles
+// blockIdx.x, blockIdx.x + gridDim.x, ... as one continuous stream of k-slabs:
+// the refills run ahead into the next tile's first slabs while this tile's
+// last slabs and epilogue run, so a short-K tile pays no TMA round trip at its
+// start (one tile per CTA otherwise).
+template <class Cfg, bool ACC, bool PERSIST = false>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     dmma_tma_kernel(double* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                     int64_t tiles_m, int64_t tiles_n, const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b) {
+  static_assert(!PERSIST || Cfg::REFILL == 1, "the persistent stream refills from the last warp");
   extern __shared__ __align__(16) unsigned char tm_raw[];
   // swizzle-128B destinations must be 1024-byte aligned
   // (offset from tm_raw rather than integer rounding of the pointer, so the
@@ -94,12 +100,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   uint64_t* empty = full + Cfg::STAGES;  // one arrival per warp when it is done with a slab
   unsigned* done_warps = reinterpret_cast<unsigned*>(empty + Cfg::STAGES);  // REFILL 1
 
-  const int64_t pid = blockIdx.x;
-  const int64_t width = Cfg::GM * tiles_n;
-  const int64_t first_m = (pid / width) * Cfg::GM;
-  const int64_t gsize = (tiles_m - first_m) < Cfg::GM ? (tiles_m - first_m) : Cfg::GM;
-  const int64_t m0 = (first_m + (pid % width) % gsize) * Cfg::BM;
-  const int64_t n0 = ((pid % width) / gsize) * Cfg::BN;
+  // origin of this CTA's local tile `lt` (row-tile raster groups of GM); the
+  // launcher keeps tile indices below 2^31, so 32-bit divisions suffice
+  auto origin = [&](int64_t lt, int64_t& m0, int64_t& n0) {
+    const uint32_t pid = blockIdx.x + (PERSIST ? (uint32_t)lt * gridDim.x : 0u);
+    const uint32_t width = Cfg::GM * (uint32_t)tiles_n;
+    const uint32_t first_m = (pid / width) * Cfg::GM;
+    const uint32_t gsize = ((uint32_t)tiles_m - first_m) < Cfg::GM ? ((uint32_t)tiles_m - first_m) : Cfg::GM;
+    const uint32_t r = pid % width;
+    m0 = (int64_t)(first_m + r % gsize) * Cfg::BM;
+    n0 = (int64_t)(r / gsize) * Cfg::BN;
+  };
+  const int64_t my_tiles =
+      PERSIST ? (tiles_m * tiles_n - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x : 1;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / (Cfg::BN / Cfg::WN)) * Cfg::WM, wn0 = (warp % (Cfg::BN / Cfg::WN)) * Cfg::WN;
@@ -116,20 +129,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   }
   __syncthreads();
 
+  // slab s of the CTA's stream: k-slab s % KT of local tile s / KT
   const int64_t KT = (K + Cfg::BK - 1) / Cfg::BK;
-  auto issue = [&](int stage, int64_t kt) {  // one thread
+  const int64_t total = my_tiles * KT;
+  auto issue = [&](int stage, int64_t s) {  // one thread
+    int64_t tm0 = 0, tn0 = 0;
+    // (PERSIST: the launcher keeps each CTA's slab count below 2^31)
+    origin(PERSIST ? (uint32_t)s / (uint32_t)KT : 0, tm0, tn0);
+    const int64_t kt = PERSIST ? (uint32_t)s % (uint32_t)KT : s;
     unsigned char* st = base + stage * Cfg::STAGE_BYTES;
     mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-    load_2d(st, &map_a, (int)(kt * Cfg::BK), (int)m0, &full[stage]);
+    load_2d(st, &map_a, (int)(kt * Cfg::BK), (int)tm0, &full[stage]);
 #pragma unroll
     for (int j = 0; j < Cfg::BN / 16; j++)
-      load_2d(st + Cfg::A_BYTES + j * 2048, &map_b, (int)(n0 + 16 * j), (int)(kt * Cfg::BK),
+      load_2d(st + Cfg::A_BYTES + j * 2048, &map_b, (int)(tn0 + 16 * j), (int)(kt * Cfg::BK),
                   &full[stage]);
   };
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < Cfg::STAGES; s++)
-      if (s < KT) issue(s, s);
+      if (s < total) issue(s, s);
   }
 
   // per-thread fragment offsets (bytes within a stage), fixed for the kernel
@@ -142,112 +161,126 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   int b_col[Cfg::NI];
 #pragma unroll
   for (int ni = 0; ni < Cfg::NI; ni++) b_col[ni] = wn0 + 16 * (ni >> 1) + pi_col(g, ni & 1);
+  const bool pair_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(c) % 16 == 0);
 
-  // accumulator (mi, ni, q) is C element (a_row[mi][q>>1], pi(2t + (q&1)))
-  double acc[Cfg::MI][Cfg::NI][4];
+#pragma unroll 1
+  for (int64_t lt = 0; lt < my_tiles; lt++) {
+    int64_t m0, n0;
+    origin(lt, m0, n0);
+    // accumulator (mi, ni, q) is C element (a_row[mi][q>>1], pi(2t + (q&1)))
+    double acc[Cfg::MI][Cfg::NI][4];
 #pragma unroll
-  for (int mi = 0; mi < Cfg::MI; mi++)
-#pragma unroll
-    for (int ni = 0; ni < Cfg::NI; ni++)
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        if (ACC) {
-          const int64_t row = m0 + a_row[mi][q >> 1];
-          const int64_t col = n0 + wn0 + 16 * (ni >> 1) + pi_col(2 * t, ni & 1) + (q & 1);
-          acc[mi][ni][q] = (row < M && col < N) ? c[row * ldc + col] : 0.0;
-        } else {
-          acc[mi][ni][q] = 0.0;
-        }
-      }
-
-  // No block-wide barrier in the main loop: warps release a slab through its
-  // `empty` mbarrier, and thread 0 refills the slab consumed one iteration
-  // earlier (so it rarely waits), keeping STAGES-2 slabs in flight ahead.
-  for (int64_t kt = 0; kt < KT; kt++) {
-    const int stage = (int)(kt % Cfg::STAGES);
-    mbar_wait(&full[stage], (unsigned)((kt / Cfg::STAGES) & 1));
-    const unsigned char* as = base + stage * Cfg::STAGE_BYTES;
-    const unsigned char* bs = as + Cfg::A_BYTES;
-#pragma unroll
-    for (int kk = 0; kk < Cfg::BK; kk += 4) {
-      double af[Cfg::MI][2], bf[Cfg::NI];
-#pragma unroll
-      for (int mi = 0; mi < Cfg::MI; mi++) {
-        af[mi][0] = *reinterpret_cast<const double*>(as + a_off(a_row[mi][0], kk + t));
-        af[mi][1] = *reinterpret_cast<const double*>(as + a_off(a_row[mi][1], kk + t));
-      }
+    for (int mi = 0; mi < Cfg::MI; mi++)
 #pragma unroll
       for (int ni = 0; ni < Cfg::NI; ni++)
-        bf[ni] = *reinterpret_cast<const double*>(bs + b_off(kk + t, b_col[ni]));
 #pragma unroll
-      for (int mi = 0; mi < Cfg::MI; mi++)
-#pragma unroll
-        for (int ni = 0; ni < Cfg::NI; ni++) dmma_step(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
-    }
-    if constexpr (Cfg::REFILL == 1) {
-      // count this warp out of the stage (its reads ordered before the async
-      // proxy's refill); the last warp out refills it with slab kt + STAGES
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        unsigned before;
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                     : "=r"(before)
-                     : "r"(tma::smem_addr(&done_warps[stage]))
-                     : "memory");
-        if (before == Cfg::WARPS - 1) {
-          done_warps[stage] = 0;  // before the refill's expect_tx arrive (a release)
-          if (kt + Cfg::STAGES < KT) issue(stage, kt + Cfg::STAGES);
+        for (int q = 0; q < 4; q++) {
+          if (ACC) {
+            const int64_t row = m0 + a_row[mi][q >> 1];
+            const int64_t col = n0 + wn0 + 16 * (ni >> 1) + pi_col(2 * t, ni & 1) + (q & 1);
+            acc[mi][ni][q] = (row < M && col < N) ? c[row * ldc + col] : 0.0;
+          } else {
+            acc[mi][ni][q] = 0.0;
+          }
         }
-      }
-    } else {
-      tma::release_stage(&empty[stage], lane);
-      // refill the slab of iteration kt-1 with k-slab kt-1+STAGES
-      if (tid == 0 && kt >= 1 && kt - 1 + Cfg::STAGES < KT) {
-        const int ps = (int)((kt - 1) % Cfg::STAGES);
-        mbar_wait(&empty[ps], (unsigned)(((kt - 1) / Cfg::STAGES) & 1));
-        issue(ps, kt - 1 + Cfg::STAGES);
-      }
-    }
-  }
 
-  // ---- epilogue: accumulator (q&1) of MMA column 2t -> tile columns pi(2t), pi(2t+1)
-  const bool pair_ok = (ldc % 2 == 0) && (reinterpret_cast<uintptr_t>(c) % 16 == 0);
+    // No block-wide barrier in the main loop: warps release a slab through its
+    // `empty` mbarrier (REFILL 0: thread 0 refills the slab consumed one
+    // iteration earlier) or the last warp out refills it (REFILL 1), keeping
+    // up to STAGES slabs in flight ahead.
+    for (int64_t kt = 0; kt < KT; kt++) {
+      const int64_t s = lt * KT + kt;
+      const int stage = (int)(s % Cfg::STAGES);
+      mbar_wait(&full[stage], (unsigned)((s / Cfg::STAGES) & 1));
+      const unsigned char* as = base + stage * Cfg::STAGE_BYTES;
+      const unsigned char* bs = as + Cfg::A_BYTES;
 #pragma unroll
-  for (int mi = 0; mi < Cfg::MI; mi++)
+      for (int kk = 0; kk < Cfg::BK; kk += 4) {
+        double af[Cfg::MI][2], bf[Cfg::NI];
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int64_t row = m0 + a_row[mi][h];
-      if (row >= M) continue;
-      double* crow = c + row * ldc;
+        for (int mi = 0; mi < Cfg::MI; mi++) {
+          af[mi][0] = *reinterpret_cast<const double*>(as + a_off(a_row[mi][0], kk + t));
+          af[mi][1] = *reinterpret_cast<const double*>(as + a_off(a_row[mi][1], kk + t));
+        }
 #pragma unroll
-      for (int ni = 0; ni < Cfg::NI; ni++) {
-        const int64_t col = n0 + wn0 + 16 * (ni >> 1) + pi_col(2 * t, ni & 1);
-        if (pair_ok && col + 1 < N) {
-          *reinterpret_cast<double2*>(crow + col) =
-              make_double2(acc[mi][ni][2 * h], acc[mi][ni][2 * h + 1]);
-        } else {
-          if (col < N) crow[col] = acc[mi][ni][2 * h];
-          if (col + 1 < N) crow[col + 1] = acc[mi][ni][2 * h + 1];
+        for (int ni = 0; ni < Cfg::NI; ni++)
+          bf[ni] = *reinterpret_cast<const double*>(bs + b_off(kk + t, b_col[ni]));
+#pragma unroll
+        for (int mi = 0; mi < Cfg::MI; mi++)
+#pragma unroll
+          for (int ni = 0; ni < Cfg::NI; ni++) dmma_step(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+      }
+      if constexpr (Cfg::REFILL == 1) {
+        // count this warp out of the stage (its reads ordered before the async
+        // proxy's refill); the last warp out refills it with slab s + STAGES
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          unsigned before;
+          asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                       : "=r"(before)
+                       : "r"(tma::smem_addr(&done_warps[stage]))
+                       : "memory");
+          if (before == Cfg::WARPS - 1) {
+            done_warps[stage] = 0;  // before the refill's expect_tx arrive (a release)
+            if (s + Cfg::STAGES < total) issue(stage, s + Cfg::STAGES);
+          }
+        }
+      } else {
+        tma::release_stage(&empty[stage], lane);
+        // refill the slab of iteration s-1 with slab s-1+STAGES
+        if (tid == 0 && s >= 1 && s - 1 + Cfg::STAGES < total) {
+          const int ps = (int)((s - 1) % Cfg::STAGES);
+          mbar_wait(&empty[ps], (unsigned)(((s - 1) / Cfg::STAGES) & 1));
+          issue(ps, s - 1 + Cfg::STAGES);
         }
       }
     }
+
+    // ---- epilogue: accumulator (q&1) of MMA column 2t -> tile columns pi(2t), pi(2t+1)
+#pragma unroll
+    for (int mi = 0; mi < Cfg::MI; mi++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t row = m0 + a_row[mi][h];
+        if (row >= M) continue;
+        double* crow = c + row * ldc;
+#pragma unroll
+        for (int ni = 0; ni < Cfg::NI; ni++) {
+          const int64_t col = n0 + wn0 + 16 * (ni >> 1) + pi_col(2 * t, ni & 1);
+          if (pair_ok && col + 1 < N) {
+            *reinterpret_cast<double2*>(crow + col) =
+                make_double2(acc[mi][ni][2 * h], acc[mi][ni][2 * h + 1]);
+          } else {
+            if (col < N) crow[col] = acc[mi][ni][2 * h];
+            if (col + 1 < N) crow[col + 1] = acc[mi][ni][2 * h + 1];
+          }
+        }
+      }
+  }
 }
 
-template <class Cfg>
+template <class Cfg, bool PERSIST = false>
 cudaError_t dmma_tma_launch(const Problem& p) {
   CUtensorMap map_a, map_b;
   if (!make_tensor_map_2d(&map_a, p.a, 8, p.M, p.K, p.lda, Cfg::BM, 16, true) ||
       !make_tensor_map_2d(&map_b, p.b, 8, p.K, p.N, p.ldb, Cfg::BK, 16, true))
     return cudaErrorInvalidValue;
-  auto kern = p.accumulate ? dmma_tma_kernel<Cfg, true> : dmma_tma_kernel<Cfg, false>;
+  auto kern = p.accumulate ? dmma_tma_kernel<Cfg, true, PERSIST> : dmma_tma_kernel<Cfg, false, PERSIST>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles_m = (p.M + Cfg::BM - 1) / Cfg::BM, tiles_n = (p.N + Cfg::BN - 1) / Cfg::BN;
   const int64_t tiles = tiles_m * tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  kern<<<(unsigned)tiles, Cfg::THREADS, Cfg::SMEM, p.stream>>>(
+  int64_t grid = tiles;
+  if (PERSIST) {
+    const int64_t slots = (int64_t)sm_count() * Cfg::MINB;
+    grid = tiles < slots ? tiles : slots;
+    const int64_t per_cta = (tiles + grid - 1) / grid * ((p.K + Cfg::BK - 1) / Cfg::BK);
+    if (per_cta >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
+  }
+  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, p.stream>>>(
       static_cast<double*>(p.c), p.M, p.N, p.K, p.ldc, tiles_m, tiles_n, map_a, map_b);
   count_launch();
   return cudaGetLastError();
