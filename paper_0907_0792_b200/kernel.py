@@ -356,6 +356,7 @@ def execute_sequential(plan: KernelPlan, a: MoaArray, b: MoaArray, ops: OpPair =
 
 
 _HUGE_PAGE = 2 << 20
+_PINNED_RESULT_BYTES = 256 << 10  # host_runtime.cu kDirectBytes
 _TRACE = bool(__import__("os").environ.get("MOA_HOST_TRACE"))
 
 
@@ -368,11 +369,15 @@ def host_empty(n: int, dtype) -> np.ndarray:
     against 0.39 s per GiB for cudaHostAlloc on a B200 host,
     profiles/r02_host_probe.json), so the result's copy-back runs at link
     speed; when the array is garbage-collected the block returns to the cache
-    and the next result of a similar size reuses it.  Small results are plain
-    numpy memory."""
+    and the next result of a similar size reuses it.  Results from 256 KiB up
+    take such a block too (one 2 MiB page at least): below that the executor
+    copies pageable memory directly, above it a pageable result would be
+    staged through its copy threads, while a page-locked one of <= 1 MiB is
+    written by the kernel itself (csrc/host_exec.cu direct_out_bytes).
+    Smaller results are plain numpy memory."""
     dt = np.dtype(dtype)
     nbytes = n * dt.itemsize
-    if nbytes < 2 * _HUGE_PAGE:
+    if nbytes < _PINNED_RESULT_BYTES:
         return np.empty(n, dt)
     ptr = _native.host_alloc(nbytes)
     if not ptr:  # pragma: no cover - host out of memory

@@ -340,7 +340,7 @@ def test_short_lived_threads_reuse_pooled_queues(rng):
 
 
 def test_host_result_blocks_are_page_locked_and_reused(rng):
-    """Public-API results above 4 MiB live in moa_host_alloc blocks: huge-page
+    """Public-API results from 256 KiB up live in moa_host_alloc blocks: huge-page
     backed and page-locked (the copy-back needs no staging), returned to the
     cache when the array dies and reused by the next result of that size."""
     import gc
@@ -358,6 +358,10 @@ def test_host_result_blocks_are_page_locked_and_reused(rng):
     out2 = moa.outer(MoaArray((1000,), y[:1000]), MoaArray((3000,), y))
     assert out2.data.ctypes.data == ptr  # the idle block was reused
     assert_bits_equal(out2.data, (np.multiply.outer(y[:1000], y) + 0.0).ravel())
+    # a 320 KiB result is page-locked too (kernel stores straight into it)
+    small = moa.outer(MoaArray((200,), x[:200]), MoaArray((200,), y[:200]))
+    assert torch.from_numpy(small.data).is_pinned()
+    assert_bits_equal(small.data, (np.multiply.outer(x[:200], y[:200]) + 0.0).ravel())
     # the raw allocator: distinct live blocks, reuse after free
     p1, p2 = _native.host_alloc(5 << 20), _native.host_alloc(5 << 20)
     assert p1 and p2 and p1 != p2

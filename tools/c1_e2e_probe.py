@@ -48,6 +48,21 @@ for _ in range(calls):
 ts.sort()
 print(f"{m}x{k}x{n} e2e C ABI (direct-out limit {os.environ.get('MOA_HOST_DIRECT_OUT_BYTES', 'default')}): median {ts[len(ts) // 2]:.1f} us, best {ts[0]:.1f} us, p90 {ts[int(len(ts) * 0.9)]:.1f} us")
 
+import paper_0907_0792_b200 as moa  # noqa: E402
+from paper_0907_0792_b200 import MoaArray  # noqa: E402
+
+for label, A, B in (("pinned MoaArrays", MoaArray._wrap((m, k), a), MoaArray._wrap((k, n), b)),
+                    ("numpy MoaArrays", MoaArray((m, k), a.copy()), MoaArray((k, n), b.copy()))):
+    for _ in range(20):
+        moa.inner(A, B)
+    ts = []
+    for _ in range(calls):
+        t0 = time.perf_counter()
+        moa.inner(A, B)
+        ts.append((time.perf_counter() - t0) * 1e6)
+    ts.sort()
+    print(f"{m}x{k}x{n} e2e moa.inner on {label}: median {ts[len(ts) // 2]:.1f} us, best {ts[0]:.1f} us")
+
 if "notrace" in sys.argv:
     sys.exit(0)
 os.environ["MOA_HOST_TRACE"] = "1"
