@@ -130,6 +130,16 @@ size_t direct_out_bytes() {
   return v;
 }
 
+// $MOA_HOST_ROW_PARTS=0 turns the row-part pipeline of large single-block
+// results off (one kernel, then the copy-out), for comparisons
+bool row_parts_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("MOA_HOST_ROW_PARTS");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 // $MOA_HOST_TRACE=1: one stderr line per call with the host-side phase times
 struct Trace {
   const bool on = std::getenv("MOA_HOST_TRACE") != nullptr;
@@ -319,6 +329,66 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     char* b_dev = static_cast<char*>(ss.alloc(1, (size_t)(K > 0 ? b_span : 0) * esz, sb));
     char* c_dev = c_direct ? c_direct : static_cast<char*>(ss.alloc(2, out_bytes, st));
     if (ss.err != cudaSuccess) return fail_cuda(ss.err, "device buffers");
+    // A large result into page-locked res: the product runs as row parts,
+    // each part's rows copied out on their own queue while the next part
+    // computes (its A rows, and C rows when accumulating, copied in just
+    // before it), so the copy-out starts after the first part instead of the
+    // whole kernel.  Row parts never change the route or a bit (capi.cu
+    // route() depends on K only).
+    const bool parts = !c_direct && r_pin && rows >= 4 * kRowAlign && out_bytes >= (64ull << 20) &&
+                       row_parts_enabled();
+    if (parts) {
+      // every copy in rides one queue in order (B, then each part's A rows /
+      // C rows), each part's kernel waits for its own rows only
+      cudaStream_t si = q.s_in;
+      cudaEvent_t allocated = ss.event();  // buffers drawn on st are ready on si too
+      ss.check(cudaEventRecord(allocated, st));
+      ss.check(cudaStreamWaitEvent(si, allocated, 0));
+      if (K > 0) {
+        if (!a_dense) copy_a(a_dev, 0, rows, 0, K, si);
+        copy_b(b_dev, 0, K, si);
+      }
+      int64_t per = (rows + 3) / 4;
+      per += (kRowAlign - per % kRowAlign) % kRowAlign;
+      for (int64_t r0 = 0; r0 < rows && ss.err == cudaSuccess; r0 += per) {
+        const int64_t nr = r0 + per < rows ? per : rows - r0;
+        char* c_part = c_dev + (size_t)(r0 * N) * esz;
+        char* a_part = nullptr;
+        if (K > 0) {
+          if (a_dense) {
+            a_part = a_dev + (size_t)(r0 * K) * esz;
+            copy_a(a_part, r0, nr, 0, K, si);
+          } else {
+            a_part = a_dev + (size_t)(r0 * lda) * esz;
+          }
+        }
+        if (acc)
+          ss.check(moa::host::h2d(device, c_part, (size_t)N * esz, c_rows + (size_t)r0 * c_pitch,
+                                  c_pitch, (size_t)N * esz, (size_t)nr, true, si));
+        cudaEvent_t in = ss.event();
+        ss.check(cudaEventRecord(in, si));
+        ss.check(cudaStreamWaitEvent(st, in, 0));
+        if (ss.err != cudaSuccess) break;
+        const int rc = moa_product_rows(dtype, c_part, a_part, K > 0 ? b_dev : nullptr, nr, K, N,
+                                        K > 0 ? lda : 0, K > 0 ? ldb : N, N, combine_code,
+                                        reduce_code, 0, 1, flags, st);
+        if (rc != 0) {
+          ss.err = cudaErrorUnknown;  // drain before the queues are reused; message already set
+          return rc;
+        }
+        cudaEvent_t done = ss.event();
+        ss.check(cudaEventRecord(done, st));
+        ss.check(cudaStreamWaitEvent(q.s_out, done, 0));
+        ss.check(moa::host::d2h(device, c_rows + (size_t)r0 * c_pitch, c_pitch, c_part,
+                                (size_t)N * esz, (size_t)N * esz, (size_t)nr, true, q.s_out));
+      }
+      tr.mark("parts_issued");
+      ss.check(cudaStreamSynchronize(q.s_out));
+      ss.check(cudaStreamSynchronize(st));
+      tr.mark("out_parts");
+      if (ss.err != cudaSuccess) return fail_cuda(ss.err, "host product");
+      return 0;
+    }
     if (K > 0) {
       copy_a(a_dev, 0, rows, 0, K, st);
       copy_b(b_dev, 0, K, sb);
@@ -345,22 +415,6 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     if (c_direct) {
       ss.check(cudaStreamSynchronize(st));
       tr.mark("out_direct");
-    } else if (r_pin && rows >= 4 && out_bytes >= (64ull << 20)) {
-      // a large result leaves over four copy queues, which draw a little
-      // more of the host link than one (tools/e2e_probe.py: 54.8 -> 56.9 GB/s)
-      cudaEvent_t done = ss.event();
-      ss.check(cudaEventRecord(done, st));
-      const int64_t per = (rows + 3) / 4;
-      cudaStream_t qs[4] = {st, q.s_aux[0], q.s_aux[1], q.s_aux[2]};
-      for (int i = 0; i < 4; i++) {
-        const int64_t r0 = i * per, r1 = (i + 1) * per < rows ? (i + 1) * per : rows;
-        if (r0 >= r1) break;
-        if (i > 0) ss.check(cudaStreamWaitEvent(qs[i], done, 0));
-        ss.check(moa::host::d2h(device, c_rows + (size_t)r0 * c_pitch, c_pitch,
-                                c_dev + (size_t)(r0 * N) * esz, (size_t)N * esz, (size_t)N * esz,
-                                (size_t)(r1 - r0), true, qs[i]));
-      }
-      for (cudaStream_t x : qs) ss.check(cudaStreamSynchronize(x));
     } else {
       ss.check(moa::host::d2h(device, c_rows, c_pitch, c_dev, (size_t)N * esz, (size_t)N * esz,
                               (size_t)rows, r_pin, st));

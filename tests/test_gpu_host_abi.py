@@ -265,6 +265,35 @@ def test_direct_out_into_page_locked_res(dt, rng):
 
 
 @pytest.mark.parametrize("acc", [False, True])
+def test_row_parts_into_page_locked_res(acc, rng):
+    """Results of >= 64 MiB into page-locked res run as four row parts whose
+    copy-out overlaps the next part's kernel: the bits of the device entry
+    point for the DMMA, tropical and outer routes, a strided row set (only its
+    rows written) and overlapping A rows (the whole span of A goes first)."""
+    m, k, n = 16384, 33, 1024
+    cases = [(np.float64, moa.MUL_ADD, 1, k), (np.float64, moa.MUL_ADD, 2, k),
+             (np.float32, op_pair("add", "min"), 1, k), (np.float64, op_pair("max", "add"), 1, 20)]
+    for dt, ops, step, lstride in cases:   # every row set >= 64 MiB of result
+        a = _operands(rng, (m - 1) * lstride + k, dt)
+        b = _operands(rng, k * n, dt)
+        plan = KernelPlan("inner", m, k, n, lstride, n, n, (m, n))
+        res0 = _operands(rng, m * n, dt)
+        kw = dict(step=step, accumulate=acc)
+        want = _device_result(plan, res0, a, b, ops, **kw)
+        got = _pinned_like(res0)
+        launch_host(plan, got, _pinned_like(a), _pinned_like(b), ops, **kw)
+        assert_bits_equal(got, want, f"{dt.__name__} {ops} step={step} lstride={lstride} acc={acc}")
+    # outer product (K = 1): 8192 x 2048 f64 = 128 MiB
+    x, y = _operands(rng, 8192, np.float64), _operands(rng, 2048, np.float64)
+    plan = plan_outer((8192,), (2048,))
+    res0 = _operands(rng, 8192 * 2048, np.float64)
+    want = _device_result(plan, res0, x, y, moa.MUL_ADD, accumulate=acc)
+    got = _pinned_like(res0)
+    launch_host(plan, got, _pinned_like(x), _pinned_like(y), moa.MUL_ADD, accumulate=acc)
+    assert_bits_equal(got, want, f"outer acc={acc}")
+
+
+@pytest.mark.parametrize("acc", [False, True])
 def test_pageable_staging_equals_page_locked(acc, rng):
     """Pageable host buffers above the direct-copy size are staged through
     page-locked slots by the executor's copy threads (host_runtime.cu): many
