@@ -24,6 +24,7 @@
 // events and small device buffers come from a per-device pool of queue sets
 // (one per concurrent caller), large block buffers from a private device
 // memory pool, so a call costs a few API calls beyond its copies and kernels.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -85,6 +86,7 @@ std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K, int64
   if (first <= 0 || last <= 0) return {{0, rows}};
   const int64_t mid = rows - first - last;
   int64_t nmid = 3;
+  if (const char* e = std::getenv("MOA_HOST_MID_BLOCKS")) nmid = std::max<int64_t>(1, std::atoll(e));
   const int64_t cap_aligned = cap_rows - cap_rows % kRowAlign;  // whole tiles per block
   if (cap_aligned >= kRowAlign && (mid + nmid - 1) / nmid > cap_aligned)
     nmid = (mid + cap_aligned - 1) / cap_aligned;
