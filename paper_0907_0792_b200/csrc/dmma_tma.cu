@@ -80,17 +80,19 @@ __device__ __forceinline__ int b_off(int k, int n) {
   return (n >> 4) * 2048 + k * 128 + (((((n & 15) >> 1) ^ k) & 7) << 4) + ((n & 1) << 3);
 }
 
-// PERSIST: gridDim.x <= tiles CTAs (one per resident slot), each taking tiles
-// blockIdx.x, blockIdx.x + gridDim.x, ... as one continuous stream of k-slabs:
-// the refills run ahead into the next tile's first slabs while this tile's
-// last slabs and epilogue run, so a short-K tile pays no TMA round trip at its
-// start (one tile per CTA otherwise).
-template <class Cfg, bool ACC, bool PERSIST = false>
+// TPC (tiles per CTA): 1 = one tile per CTA (production); 0 = persistent,
+// gridDim.x <= tiles CTAs (one per resident slot) taking tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ...; n >= 2 = tiles n*blockIdx.x .. n*blockIdx.x+n-1.
+// A CTA with several tiles streams their k-slabs back to back: the refills
+// run ahead into the next tile's first slabs while this tile's last slabs and
+// epilogue run, so a short-K tile pays no TMA round trip at its start.
+template <class Cfg, bool ACC, int TPC = 1>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     dmma_tma_kernel(double* __restrict__ c, int64_t M, int64_t N, int64_t K, int64_t ldc,
                     int64_t tiles_m, int64_t tiles_n, const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b) {
-  static_assert(!PERSIST || Cfg::REFILL == 1, "the persistent stream refills from the last warp");
+  static_assert(TPC == 1 || Cfg::REFILL == 1, "a multi-tile slab stream refills from the last warp");
+  constexpr bool MULTI = TPC != 1;
   extern __shared__ __align__(16) unsigned char tm_raw[];
   // swizzle-128B destinations must be 1024-byte aligned
   // (offset from tm_raw rather than integer rounding of the pointer, so the
@@ -103,7 +105,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   // origin of this CTA's local tile `lt` (row-tile raster groups of GM); the
   // launcher keeps tile indices below 2^31, so 32-bit divisions suffice
   auto origin = [&](int64_t lt, int64_t& m0, int64_t& n0) {
-    const uint32_t pid = blockIdx.x + (PERSIST ? (uint32_t)lt * gridDim.x : 0u);
+    const uint32_t pid = TPC == 0   ? blockIdx.x + (uint32_t)lt * gridDim.x
+                         : TPC == 1 ? blockIdx.x
+                                    : blockIdx.x * (uint32_t)TPC + (uint32_t)lt;
     const uint32_t width = Cfg::GM * (uint32_t)tiles_n;
     const uint32_t first_m = (pid / width) * Cfg::GM;
     const uint32_t gsize = ((uint32_t)tiles_m - first_m) < Cfg::GM ? ((uint32_t)tiles_m - first_m) : Cfg::GM;
@@ -111,8 +115,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     m0 = (int64_t)(first_m + r % gsize) * Cfg::BM;
     n0 = (int64_t)(r / gsize) * Cfg::BN;
   };
-  const int64_t my_tiles =
-      PERSIST ? (tiles_m * tiles_n - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x : 1;
+  int64_t my_tiles = 1;
+  if constexpr (TPC == 0) {
+    my_tiles = (tiles_m * tiles_n - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x;
+  } else if constexpr (TPC > 1) {
+    const int64_t rest = tiles_m * tiles_n - (int64_t)blockIdx.x * TPC;
+    my_tiles = rest < TPC ? rest : TPC;
+  }
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / (Cfg::BN / Cfg::WN)) * Cfg::WM, wn0 = (warp % (Cfg::BN / Cfg::WN)) * Cfg::WN;
@@ -134,9 +143,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   const int64_t total = my_tiles * KT;
   auto issue = [&](int stage, int64_t s) {  // one thread
     int64_t tm0 = 0, tn0 = 0;
-    // (PERSIST: the launcher keeps each CTA's slab count below 2^31)
-    origin(PERSIST ? (uint32_t)s / (uint32_t)KT : 0, tm0, tn0);
-    const int64_t kt = PERSIST ? (uint32_t)s % (uint32_t)KT : s;
+    // (MULTI: the launcher keeps each CTA's slab count below 2^31)
+    origin(MULTI ? (uint32_t)s / (uint32_t)KT : 0, tm0, tn0);
+    const int64_t kt = MULTI ? (uint32_t)s % (uint32_t)KT : s;
     unsigned char* st = base + stage * Cfg::STAGE_BYTES;
     mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
     load_2d(st, &map_a, (int)(kt * Cfg::BK), (int)tm0, &full[stage]);
@@ -260,13 +269,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   }
 }
 
-template <class Cfg, bool PERSIST = false>
+template <class Cfg, int TPC = 1>
 cudaError_t dmma_tma_launch(const Problem& p) {
   CUtensorMap map_a, map_b;
   if (!make_tensor_map_2d(&map_a, p.a, 8, p.M, p.K, p.lda, Cfg::BM, 16, true) ||
       !make_tensor_map_2d(&map_b, p.b, 8, p.K, p.N, p.ldb, Cfg::BK, 16, true))
     return cudaErrorInvalidValue;
-  auto kern = p.accumulate ? dmma_tma_kernel<Cfg, true, PERSIST> : dmma_tma_kernel<Cfg, false, PERSIST>;
+  auto kern = p.accumulate ? dmma_tma_kernel<Cfg, true, TPC> : dmma_tma_kernel<Cfg, false, TPC>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
   if (e != cudaSuccess) return e;
@@ -274,9 +283,13 @@ cudaError_t dmma_tma_launch(const Problem& p) {
   const int64_t tiles = tiles_m * tiles_n;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   int64_t grid = tiles;
-  if (PERSIST) {
+  if constexpr (TPC == 0) {
     const int64_t slots = (int64_t)sm_count() * Cfg::MINB;
     grid = tiles < slots ? tiles : slots;
+  } else if constexpr (TPC > 1) {
+    grid = (tiles + TPC - 1) / TPC;
+  }
+  if (TPC != 1) {
     const int64_t per_cta = (tiles + grid - 1) / grid * ((p.K + Cfg::BK - 1) / Cfg::BK);
     if (per_cta >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
   }

@@ -1,6 +1,6 @@
 // The TMA-staged DMMA kernel (csrc/dmma_tma.cu): one tile per CTA vs the
-// persistent form (one CTA per resident slot streaming its tiles' k-slabs
-// back to back) across K, CUDA-event times (best of reps) and bit-equality.
+// persistent form (one CTA per resident slot) and 2 / 4 consecutive tiles per
+// CTA, each CTA streaming its tiles' k-slabs back to back, across K, CUDA-event times (best of reps) and bit-equality.
 // Prints JSON lines.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr \
 //   -I paper_0907_0792_b200/csrc -I include -o tools/tune_dmma_persist tools/tune_dmma_persist.cu \
@@ -29,15 +29,15 @@ __global__ void fill_u(double* x, int64_t n, unsigned seed) {
   }
 }
 
-template <bool PERSIST>
+template <int TPC>
 double run(Problem p, int reps) {
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
-  CK((dmma_tma_launch<TmaMain, PERSIST>(p)));
+  CK((dmma_tma_launch<TmaMain, TPC>(p)));
   CK(cudaDeviceSynchronize());
   double best = 1e30;
   for (int r = 0; r < reps; r++) {
-    CK(cudaEventRecord(a)); CK((dmma_tma_launch<TmaMain, PERSIST>(p))); CK(cudaEventRecord(b));
+    CK(cudaEventRecord(a)); CK((dmma_tma_launch<TmaMain, TPC>(p))); CK(cudaEventRecord(b));
     CK(cudaEventSynchronize(b));
     float ms; CK(cudaEventElapsedTime(&ms, a, b)); best = ms < best ? ms : best;
   }
@@ -61,19 +61,27 @@ int main(int argc, char** argv) {
     p.lda = K; p.ldb = N; p.ldc = N; p.combine = 2; p.reduce = 0; p.stream = 0;
     p.accumulate = acc;
     const int reps = argc > 3 ? atoi(argv[3]) : acc ? 1 : (M * N * K > (int64_t)1 << 40 ? 3 : 20);
-    p.c = c0; double t0 = run<false>(p, reps);
-    p.c = c1; double t1 = run<true>(p, reps);
+    p.c = c0; double t0 = run<1>(p, reps);
     std::vector<double> h0(M * N), h1(M * N);
     CK(cudaMemcpy(h0.data(), c0, M * N * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(h1.data(), c1, M * N * 8, cudaMemcpyDeviceToHost));
-    int64_t diffs = 0;
-    for (int64_t i = 0; i < M * N; i++) diffs += memcmp(&h0[i], &h1[i], 8) != 0;
     const double fl = 2.0 * M * N * K;
-    printf("{\"M\": %lld, \"K\": %lld, \"N\": %lld, \"accumulate\": %d, \"tile_per_cta_ms\": %.4f, "
-           "\"persistent_ms\": %.4f, \"tile_per_cta_TF\": %.2f, \"persistent_TF\": %.2f, \"bit_diffs\": %lld}\n",
-           (long long)M, (long long)K, (long long)N, (int)acc, t0, t1, fl / t0 / 1e9, fl / t1 / 1e9,
-           (long long)diffs);
-    fflush(stdout);
+    printf("{\"M\": %lld, \"K\": %lld, \"N\": %lld, \"accumulate\": %d, \"tiles_per_cta\": 1, \"ms\": %.4f, \"TF\": %.2f}\n",
+           (long long)M, (long long)K, (long long)N, (int)acc, t0, fl / t0 / 1e9);
+    auto other = [&](int tpc, double t1) {
+      CK(cudaMemcpy(h1.data(), c1, M * N * 8, cudaMemcpyDeviceToHost));
+      int64_t diffs = 0;
+      for (int64_t i = 0; i < M * N; i++) diffs += memcmp(&h0[i], &h1[i], 8) != 0;
+      printf("{\"M\": %lld, \"K\": %lld, \"N\": %lld, \"accumulate\": %d, \"tiles_per_cta\": %d, \"ms\": %.4f, \"TF\": %.2f, \"bit_diffs\": %lld}\n",
+             (long long)M, (long long)K, (long long)N, (int)acc, tpc, t1, fl / t1 / 1e9, (long long)diffs);
+      fflush(stdout);
+    };
+    p.c = c1; CK(cudaMemcpy(c1, c0, 0, cudaMemcpyDeviceToDevice));
+    if (acc) fill_u<<<1184, 256>>>(c1, M * N, 3);
+    other(0, run<0>(p, reps));
+    if (acc) fill_u<<<1184, 256>>>(c1, M * N, 3);
+    other(2, run<2>(p, reps));
+    if (acc) fill_u<<<1184, 256>>>(c1, M * N, 3);
+    other(4, run<4>(p, reps));
     CK(cudaFree(a)); CK(cudaFree(b)); CK(cudaFree(c0)); CK(cudaFree(c1));
   }
   return 0;
