@@ -9,6 +9,10 @@
 // reference's execute_parallel, parallel.py:26-43) never touch each other's
 // rows.
 //
+// Products with one block of result (< 1 GiB) run in order on one queue, with
+// two refinements for page-locked res: a write-only result of <= 1 MiB is
+// stored by the kernel straight into res (no copy after the kernel), and one
+// of >= 64 MiB runs as four row parts whose copy-out overlaps the next part.
 // Large products are streamed (the public Python API's host path runs through
 // here too, kernel.execute_host): row blocks with a 3/16 first block, three middle
 // blocks and a 1/16 last block; A rows of the next block copy in on one
@@ -317,8 +321,8 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   };
 
   // ---- one block: in order on one queue (page-locked B copies in on a
-  // second queue, concurrently with A; a small write-only result goes
-  // straight into page-locked res)
+  // second queue; a small write-only result goes straight into page-locked
+  // res; a large one into page-locked res runs as row parts)
   if (blocks.size() == 1) {
     cudaStream_t st = q.s_comp;
     const size_t out_bytes = (size_t)(rows * N) * esz;
