@@ -13,9 +13,12 @@ cases = [  # (label, dtype, ops, (m, k, n), shift: 1 = misaligned A -> cp.async 
     ("dmma TMA 64x64", np.float64, moa.MUL_ADD, (4096, 256, 4096), 0),
     ("dmma TMA 16x32", np.float64, moa.MUL_ADD, (256, 1024, 256), 0),
     ("dmma cp.async", np.float64, moa.MUL_ADD, (2048, 255, 2048), 1),
-    ("tropical f32 TMA", np.float32, op_pair("add", "min"), (2048, 512, 4096), 0),
+    ("tropical f32 TMA 128x128", np.float32, op_pair("add", "min"), (2048, 512, 4096), 0),
+    ("tropical f32 TMA 64x128", np.float32, op_pair("add", "min"), (1000, 512, 1024), 0),
+    ("tropical f32 FMNMX3 128x128", np.float32, op_pair("subtract", "max"), (2048, 512, 4096), 0),
     ("tropical f32 cp.async", np.float32, op_pair("subtract", "max"), (1024, 511, 1024), 1),
-    ("int32 DPX TMA", np.int32, op_pair("add", "min"), (2048, 512, 4096), 0),
+    ("int32 DPX TMA 128x128", np.int32, op_pair("add", "min"), (2048, 512, 4096), 0),
+    ("int32 DPX TMA 64x128", np.int32, op_pair("add", "max"), (1000, 512, 1024), 0),
     ("f64 exact (add,min)", np.float64, op_pair("add", "min"), (1024, 256, 1024), 0),
     ("f32 max-times", np.float32, op_pair("multiply", "max"), (2048, 256, 2048), 0),
     ("f32 (divide,max) exact", np.float32, op_pair("divide", "max"), (1024, 256, 1024), 0),
