@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(TropTma<BMT>::THREADS, MINB)
       // (k..k+3 are one swizzle chunk) per row — 16 shared loads per 256
       // (a, b) pairs instead of 24
       const int nquads = kend >> 2;
-#pragma unroll 1
+#pragma unroll UNR
       for (int kq = 0; kq < nquads; kq++) {
         const int k = 4 * kq;
         const int aoff = ((kq ^ ty) & 7) << 4;
