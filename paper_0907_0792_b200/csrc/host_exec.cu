@@ -14,7 +14,7 @@
 // stored by the kernel straight into res (no copy after the kernel), and one
 // of >= 64 MiB runs as four row parts whose copy-out overlaps the next part.
 // Large products are streamed (the public Python API's host path runs through
-// here too, kernel.execute_host): row blocks with a 3/16 first block, three middle
+// here too, kernel.execute_host): row blocks with a 4/16 first block, three middle
 // blocks and a 1/16 last block; A rows of the next block copy in on one
 // stream while the current block computes on another and the previous block's
 // rows copy out on a third, double-buffered.  Every row needs all of B, so B
@@ -66,7 +66,7 @@ int64_t max_block_bytes() {
 
 // Row blocks of the set: one block below 1 GiB of result; outer products (and
 // K = 0) in equal blocks of at most max_block_bytes(), whose copy-out overlaps
-// the next block's kernel; inner products as a 3/16 first block (computed per
+// the next block's kernel; inner products as a 4/16 first block (computed per
 // k-chunk of B), middle blocks, a 1/16 last block, every block within
 // max_block_bytes() so device memory stays bounded (two slots of each buffer).
 std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K, int64_t row_bytes) {
@@ -80,7 +80,13 @@ std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K, int64
     for (int64_t r = 0; r < rows; r += size) out.push_back({r, r + size < rows ? r + size : rows});
     return out;
   }
-  int64_t first = rows * 3 / 16, last = rows / 16;
+  // first block: 4/16 of the rows (c4 through the C ABI 257.7 ms with 3/16,
+  // 254.0 with 4/16, 255.0 with 5/16; c5 215.4 / 215.5 / 217.2 ms,
+  // profiles/r02_e2e_first_block.log): long enough that B and the next
+  // block's A rows are in before it ends; $MOA_HOST_FIRST_16THS overrides it
+  int64_t first_16ths = 4;
+  if (const char* e = std::getenv("MOA_HOST_FIRST_16THS")) first_16ths = std::max<int64_t>(1, std::atoll(e));
+  int64_t first = rows * first_16ths / 16, last = rows / 16;
   if (cap_rows >= kRowAlign) {
     first = first < cap_rows ? first : cap_rows;
     last = last < cap_rows ? last : cap_rows;

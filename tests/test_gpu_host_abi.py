@@ -134,7 +134,7 @@ def test_host_entry_outer_fill_and_page_locked_buffers(rng):
                                     (np.float32, op_pair("add", "min")),
                                     (np.float32, op_pair("multiply", "add"))])
 def test_host_entry_streamed_blocks_equal_one_launch(dt, ops, rng):
-    """Results of >= 1 GiB run the streamed schedule (3/16 first block computed
+    """Results of >= 1 GiB run the streamed schedule (4/16 first block computed
     per k-chunk of B, middle blocks, 1/16 last block; float32 sums take B
     whole): bitwise equal to one device launch."""
     torch = _torch()
@@ -180,7 +180,7 @@ def test_host_entry_argument_errors(rng):
 def test_host_entry_bounded_blocks(monkeypatch, rng):
     """Every block's A and C rows stay within $MOA_HOST_BLOCK_BYTES (4 GiB by
     default): a small cap forces many blocks for an outer product (equal
-    blocks) and for a sub-GiB inner product (3/16 first block per k-chunk,
+    blocks) and for a sub-GiB inner product (4/16 first block per k-chunk,
     extra middle blocks); results bitwise equal one device launch."""
     torch = _torch()
     monkeypatch.setenv("MOA_HOST_BLOCK_BYTES", str(3 << 20))  # 3 MiB
@@ -190,7 +190,7 @@ def test_host_entry_bounded_blocks(monkeypatch, rng):
     assert_bits_equal(res, np.subtract.outer(x, y).ravel())
     for ops, dt in ((moa.MUL_ADD, np.float64), (op_pair("add", "min"), np.float32),
                     (op_pair("divide", "max"), np.float64)):
-        m, k, n = 2100, 96, 640  # 6.9 MiB of A+C rows: 384-row first block, 128-row last
+        m, k, n = 2100, 96, 640  # 6.9 MiB of A+C rows: 512-row first block, 128-row last
         a = (rng.random(m * k) * 100 + 1).astype(dt)
         b = (rng.random(k * n) * 100 + 1).astype(dt)
         plan = plan_inner((m, k), (k, n))
