@@ -126,6 +126,40 @@ std::vector<std::pair<int64_t, int64_t>> k_chunks(int64_t K, int chunks, int64_t
   return out;
 }
 
+// [0, K) as a ramp for the first block: a first chunk of ~K/32 (so its
+// kernel starts after a short copy), each next one 1.25x the last (B's chunk
+// plus the block's A columns copy in at >= 0.8x the speed the block computes
+// them even at c4, the most copy-heavy case: 48.8 ms of copies per 61 ms of
+// compute), inner boundaries on multiples of `align` and no chunk shorter
+// than `align` (each keeps the whole product's route).
+std::vector<std::pair<int64_t, int64_t>> ramp_chunks(int64_t K, int64_t align) {
+  if (K <= 2 * align) return {{0, K}};
+  const auto up = [&](double x) {
+    const int64_t v = (int64_t)x;
+    return std::max<int64_t>(align, (v + align - 1) / align * align);
+  };
+  std::vector<std::pair<int64_t, int64_t>> out;
+  double size = (double)K / 32;
+  for (int64_t k0 = 0; k0 < K; size *= 1.25) {
+    const int64_t s = up(size);
+    out.push_back({k0, k0 + s < K ? k0 + s : K});
+    k0 += s;
+  }
+  if (out.size() > 1 && out.back().second - out.back().first < align) {
+    out[out.size() - 2].second = K;
+    out.pop_back();
+  }
+  return out;
+}
+
+bool chunk_ramp_enabled() {  // $MOA_HOST_CHUNK_RAMP=0: eight equal chunks (round 1)
+  static const bool v = [] {
+    const char* e = std::getenv("MOA_HOST_CHUNK_RAMP");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 // Write-only single-block products with a page-locked res up to this many
 // result bytes ($MOA_HOST_DIRECT_OUT_BYTES overrides it; 0 disables) store
 // their rows straight into res through its device mapping: no device result
@@ -290,8 +324,14 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
                                   ? plan_blocks(rows, rows * N * (int64_t)esz, K, (K + N) * (int64_t)esz)
                                   : std::vector<Block>{{0, rows}};
   const bool chunked = blocks.size() > 1 && !wide && K >= 2;
-  const auto chunks = chunked ? k_chunks(K, blocks.size() >= 5 ? 8 : (int)blocks.size(), 16)
-                              : std::vector<std::pair<int64_t, int64_t>>{{0, K}};
+  // long contractions ramp their chunks (c4 through the C ABI 254.1 -> 249.6
+  // ms, c5 215.4 -> 214.0); short ones keep eight equal chunks, as a ramp's
+  // many thin first chunks each re-read and re-write the block's C rows
+  // (c3, K = 256: 20.6 vs 25.2 ms; profiles/r02_e2e_chunk_ramp.log)
+  const auto chunks = !chunked ? std::vector<std::pair<int64_t, int64_t>>{{0, K}}
+                     : (chunk_ramp_enabled() && K >= 1024)
+                         ? ramp_chunks(K, 16)
+                         : k_chunks(K, blocks.size() >= 5 ? 8 : (int)blocks.size(), 16);
 
   int64_t max_rows = 0;
   for (const Block& bl : blocks) max_rows = bl.r1 - bl.r0 > max_rows ? bl.r1 - bl.r0 : max_rows;

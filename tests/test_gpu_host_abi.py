@@ -177,6 +177,32 @@ def test_host_entry_argument_errors(rng):
                               3, 4, 3, 4, 3, 3, 2, 0, 5, 1, 0, 0)
 
 
+@pytest.mark.parametrize("dt,ops", [(np.float64, moa.MUL_ADD), (np.float32, op_pair("add", "min")),
+                                    (np.float64, op_pair("subtract", "max"))])
+def test_host_entry_ramped_k_chunks(dt, ops, monkeypatch, rng):
+    """Long contractions (K >= 1024) split the first block's k-range as a ramp
+    (~K/32 first, each next 1.25x, 16-aligned): many uneven accumulating
+    chunks, still the bits of one device launch — write-only, accumulate from
+    the identity, and a strided row set."""
+    torch = _torch()
+    monkeypatch.setenv("MOA_HOST_BLOCK_BYTES", str(2 << 20))  # forces the streamed schedule
+    m, k, n = 2100, 1100, 128   # 128-row blocks; K = 1100: a ramp of 10 chunks
+    a = (rng.random(m * k) * 100).astype(dt)
+    b = (rng.random(k * n) * 100).astype(dt)
+    plan = plan_inner((m, k), (k, n))
+    want = _device_result(plan, np.zeros(m * n, dtype=dt), a, b, ops)
+    for acc, pin in ((False, True), (True, True), (False, False)):
+        res0 = np.full(m * n, ops.reduce_identity if acc else 0, dtype=dt)
+        res = _pinned_like(res0) if pin else res0.copy()
+        launch_host(plan, res, a, b, ops, accumulate=acc)
+        assert_bits_equal(res, want, f"{dt.__name__} {ops} acc={acc} pinned={pin}")
+    res = np.full(m * n, 7, dtype=dt)
+    launch_host(plan, res, a, b, ops, start=1, step=2)
+    got, ref = res.reshape(m, n), want.reshape(m, n)
+    assert_bits_equal(got[1::2].ravel(), ref[1::2].ravel(), f"{dt.__name__} {ops} rows 1::2")
+    assert np.all(got[0::2] == 7)
+
+
 def test_host_entry_bounded_blocks(monkeypatch, rng):
     """Every block's A and C rows stay within $MOA_HOST_BLOCK_BYTES (4 GiB by
     default): a small cap forces many blocks for an outer product (equal
