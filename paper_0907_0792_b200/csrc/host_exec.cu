@@ -18,7 +18,8 @@
 // blocks and a 1/16 last block; A rows of the next block copy in on one
 // stream while the current block computes on another and the previous block's
 // rows copy out on a third, double-buffered.  Every row needs all of B, so B
-// arrives in k-slab-aligned chunks behind the first block's A rows and the
+// arrives in k-slab-aligned chunks (a ramp from ~K/32 up for K >= 1024, eight
+// equal ones below) behind the first block's A rows and the
 // first block is computed chunk by chunk as they land (MOA_FLAG_ACCUMULATE),
 // wherever the fold replays exactly under chunked accumulation (everything but
 // float32 data folded in float64).  Page-locked host buffers move with
