@@ -1,7 +1,8 @@
 """Stress the native host executor's streamed schedule: repeated
 moa_product_rows_host calls on >= 1 GiB results (pinned and pageable, write-only
-and accumulate, (x,+) f64 and (add,min) f32), each compared bitwise with one
-device launch (tools)."""
+and accumulate, (x,+) f64 and (add,min) f32, equal and ramped k-chunks) and on a
+128 MiB single-block result (row parts), each compared bitwise with one device
+launch (tools)."""
 import sys
 sys.path.insert(0, '.')
 import numpy as np, torch
@@ -11,7 +12,10 @@ from paper_0907_0792_b200.kernel import launch, launch_host, plan_inner
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 rng = np.random.default_rng(9)
 for dt, ops, (m, k, n) in ((np.float64, moa.MUL_ADD, (8192, 200, 16384)),
-                          (np.float32, op_pair("add", "min"), (16384, 200, 16384))):
+                          (np.float32, op_pair("add", "min"), (16384, 200, 16384)),
+                          (np.float64, moa.MUL_ADD, (8192, 1100, 16384)),      # ramped k-chunks
+                          (np.float32, op_pair("add", "min"), (16384, 1100, 16384)),
+                          (np.float64, op_pair("subtract", "max"), (4096, 512, 4096))):  # row parts
     a = (rng.random(m * k) * 100).astype(dt); b = (rng.random(k * n) * 100).astype(dt)
     plan = plan_inner((m, k), (k, n))
     want = torch.empty(m * n, dtype=torch.from_numpy(a[:1]).dtype, device="cuda")
