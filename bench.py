@@ -105,13 +105,15 @@ def theoretical(key: str, sm_mhz: float | None) -> dict:
     """The pipe's nominal ceiling at the run's SM clock (max clock if unsampled)."""
     mhz = sm_mhz or 1965.0
     if key == "c5":
-        # one FADD2 + one VIMNMX3 per 64 pairs of a warp; FADD2 holds the
-        # issue port two clocks (0.49/clk alone, FADD 0.95/clk, FADD+VIMNMX3
-        # 0.97/clk: profiles/r02_mb_dualissue.json), so 3 issue clocks per 64
-        # pairs on each of 4 schedulers (profiles/r02_c5_ceiling.md)
+        # 64 pairs per warp need 64 adds and 32 three-input folds: 2 FADD +
+        # 1 VIMNMX3 = 3 issue clocks (FADD2 would halve the adds' issue slots
+        # but stalls dispatch next to ALU-pipe instructions: ncu on
+        # tools/mb_dualissue.cu, profiles/r02_mb_dualissue_ncu.json), on each
+        # of 4 schedulers (profiles/r02_c5_ceiling.md)
         return {"value": round(SM_COUNT * 4 * 64 / 3 * mhz * 1e6 / 1e9, 1), "unit": "Gpairs/s",
-                "what": "issue limit: FADD2 (2 issue clocks) + VIMNMX3 (1) per 64 pairs per warp, "
-                        "4 schedulers x 148 SMs (one-clock FADD2 would give 1.5x this)",
+                "what": "issue limit: 2 FADD + 1 VIMNMX3 (3 issue clocks) per 64 pairs per warp, "
+                        "4 schedulers x 148 SMs; FADD2 next to the fold stalls dispatch, so no "
+                        "form beats it (measured)",
                 "sm_mhz": mhz}
     if key == "c2":
         return {"value": None, "unit": "GB/s", "what": "write-only ceiling measured: cudaMemset "

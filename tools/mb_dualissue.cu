@@ -34,7 +34,8 @@ __device__ __forceinline__ void imin(unsigned& x, unsigned p) { asm volatile("mi
 // V: 0 FADD2 | 1 FADD2 (scalar broadcast operand) | 2 LOP3 | 3 VIMNMX3 | 4 FADD
 //    5 FADD2 + LOP3 | 6 FADD2 + VIMNMX3 | 7 FADD + VIMNMX3 | 8 FADD + LOP3
 //    9 FADD2 + IMNMX | 10 FADD2(bcast) + VIMNMX3 | 11 FFMA | 12 FFMA + VIMNMX3
-//    13 2 FADD + VIMNMX3 | 14 FADD2 + 2 LOP3
+//    13 2 FADD + VIMNMX3 | 14 FADD2 + 2 LOP3 | 15 FADD2 + 2 FADD + 2 VIMNMX3
+//    16 FADD2 + FADD + VIMNMX3 | 17 2 FADD2 + 2 FADD + 3 VIMNMX3
 template <int V, int ITERS>
 __global__ void mix(unsigned* out, unsigned seed) {
   u64 x[NA];
@@ -66,6 +67,17 @@ __global__ void mix(unsigned* out, unsigned seed) {
       if (V == 11) ffma(f[i], fa);
       if (V == 12) { ffma(f[i], fa); vmin3(acc[i], p, q); }
       if (V == 13) { fadd(f[i], fa); fadd(f[(i + 1) % NA], fa); vmin3(acc[i], p, q); }
+      if (V == 15) {  // 1 FADD2 + 2 FADD (128 adds) + 2 VIMNMX3 per (it, i): 2 c5 units in 5 instructions
+        fadd2(x[i], inc); fadd(f[i], fa); fadd(f[(i + 1) % NA], fa);
+        vmin3(acc[i], p, q); vmin3(acc[(i + 1) % NA], q, p);
+      }
+      if (V == 16) {  // 1 FADD2 + 1 FADD + 1 VIMNMX3 (no pairing constraint): FMA/ALU mix probe
+        fadd2(x[i], inc); fadd(f[i], fa); vmin3(acc[i], p, q);
+      }
+      if (V == 17) {  // 2 FADD2 + 2 FADD + 3 VIMNMX3: 3 units in 7 instructions
+        fadd2(x[i], inc); fadd(f[i], fa); vmin3(acc[i], p, q); fadd2(x[(i + 1) % NA], inc);
+        fadd(f[(i + 1) % NA], fa); vmin3(acc[(i + 1) % NA], q, p); vmin3(acc[(i + 2) % NA], p, p);
+      }
       if (V == 14) { fadd2(x[i], inc); lop3(acc[i], acc[(i + 1) % NA]); lop3(acc[(i + 3) % NA], acc[(i + 5) % NA]); }
     }
   }
@@ -103,8 +115,9 @@ int main() {
   CK(cudaMalloc(&d, 1024));
   const char* names[] = {"fadd2", "fadd2_bcast", "lop3", "vimnmx3", "fadd",
                          "fadd2+lop3", "fadd2+vimnmx3", "fadd+vimnmx3", "fadd+lop3", "fadd2+imnmx",
-                         "fadd2_bcast+vimnmx3", "ffma", "ffma+vimnmx3", "2fadd+vimnmx3", "fadd2+2lop3"};
-  const int per_iter[] = {1, 1, 1, 1, 1, 2, 2, 2, 2, 2, 2, 1, 2, 3, 3};  // warp-instructions per (it, i)
+                         "fadd2_bcast+vimnmx3", "ffma", "ffma+vimnmx3", "2fadd+vimnmx3", "fadd2+2lop3",
+                         "fadd2+2fadd+2vimnmx3", "fadd2+fadd+vimnmx3", "2fadd2+2fadd+3vimnmx3"};
+  const int per_iter[] = {1, 1, 1, 1, 1, 2, 2, 2, 2, 2, 2, 1, 2, 3, 3, 5, 3, 7};  // warp-instructions per (it, i)
   printf("{\"sms\": %d, \"clock_mhz_attr\": %.0f, \"units\": \"warp-instr per clock per SMSP\"", sms,
          khz / 1e3);
   constexpr int IT = 4096;
@@ -136,6 +149,9 @@ int main() {
   run(12, mix<12, IT>);
   run(13, mix<13, IT>);
   run(14, mix<14, IT>);
+  run(15, mix<15, IT>);
+  run(16, mix<16, IT>);
+  run(17, mix<17, IT>);
   printf("}\n");
   return 0;
 }

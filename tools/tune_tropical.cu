@@ -4,7 +4,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
 //   -I paper_0907_0792_b200/csrc -I include -o tools/tune_tropical tools/tune_tropical.cu \
 //   paper_0907_0792_b200/csrc/tma.cu paper_0907_0792_b200/csrc/host_runtime.cu
-// Usage: tools/tune_tropical [N=16384] [reps=3] [which=0: all variants, 1: bm128 only, 2: int32 DPX bm64 vs bm128, 3: unrolled quad loop]
+// Usage: tools/tune_tropical [N=16384] [reps=3] [which=0: all variants, 1: bm128 only, 2: int32 DPX bm64 vs bm128, 3: unrolled quad loop, 4: scalar-FADD form]
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -110,6 +110,10 @@ int main(int argc, char** argv) {
   const int which = argc > 3 ? atoi(argv[3]) : 0;
   if (which == 0 || which == 1)
     variant("bm128_quad_refill1", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 2, 1, true, 128, 1, 0>(p, special); });
+  if (which == 4) {  // scalar-FADD form on both tile shapes (ncu target)
+    variant("bm128_quad_form2", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 2, 1, true, 128, 1, 2>(p, special); });
+    variant("bm64_quad_form2", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 3, 1, true, 64, 1, 2>(p, special); });
+  }
   if (which == 3) {
     variant("bm128_quad_unroll2", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 2, 2, true, 128, 1, 0>(p, special); });
     variant("bm64_quad_unroll2", [&] { return tropical_tma_launch<C_ADD, R_MIN, 2, false, 3, 2, true, 64, 1, 0>(p, special); });
