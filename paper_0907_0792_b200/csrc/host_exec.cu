@@ -86,7 +86,8 @@ std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K, int64
   // profiles/r02_e2e_first_block.log): long enough that B and the next
   // block's A rows are in before it ends; $MOA_HOST_FIRST_16THS overrides it
   int64_t first_16ths = 4;
-  if (const char* e = std::getenv("MOA_HOST_FIRST_16THS")) first_16ths = std::max<int64_t>(1, std::atoll(e));
+  if (const char* e = std::getenv("MOA_HOST_FIRST_16THS"))
+    first_16ths = std::min<int64_t>(12, std::max<int64_t>(1, std::atoll(e)));  // leaves room for the rest
   int64_t first = rows * first_16ths / 16, last = rows / 16;
   if (cap_rows >= kRowAlign) {
     first = first < cap_rows ? first : cap_rows;
@@ -96,8 +97,10 @@ std::vector<Block> plan_blocks(int64_t rows, int64_t out_bytes, int64_t K, int64
   last -= last % kRowAlign;
   if (first <= 0 || last <= 0) return {{0, rows}};
   const int64_t mid = rows - first - last;
+  if (mid <= 0) return {{0, rows}};
   int64_t nmid = 3;
-  if (const char* e = std::getenv("MOA_HOST_MID_BLOCKS")) nmid = std::max<int64_t>(1, std::atoll(e));
+  if (const char* e = std::getenv("MOA_HOST_MID_BLOCKS"))
+    nmid = std::min<int64_t>(64, std::max<int64_t>(1, std::atoll(e)));
   const int64_t cap_aligned = cap_rows - cap_rows % kRowAlign;  // whole tiles per block
   if (cap_aligned >= kRowAlign && (mid + nmid - 1) / nmid > cap_aligned)
     nmid = (mid + cap_aligned - 1) / cap_aligned;
