@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cerrno>
 #include <chrono>
 #include <cstdio>
 #include <condition_variable>
@@ -111,6 +112,7 @@ const size_t kSlotBytes = env_or("MOA_HOST_SLOT_MB", 16) << 20;
 const int kSlotsPerTransfer = (int)env_or("MOA_HOST_SLOTS", 4);
 const int kMaxSlots = (int)std::max<size_t>(kSlotsPerTransfer, (256ull << 20) / kSlotBytes);
 constexpr size_t kDirectBytes = 256ull << 10;
+constexpr size_t kPrefaultBytes = 32ull << 20;  // pageable destinations this large are prefaulted
 constexpr size_t kCacheLimit = 16ull << 20;  // per cached device buffer
 
 struct Slot {
@@ -251,10 +253,43 @@ void pack(char* slot, const char* host, size_t hp, const Chunk& ch, bool to_slot
   });
 }
 
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23  // Linux 5.14
+#endif
+
+// A large pageable destination (a freshly allocated numpy result: untouched
+// 4 KiB pages) is faulted in before the copy-back reaches it: huge pages
+// advised over its 2 MiB-aligned interior, then populated writable by the
+// copy threads in parallel (MADV_POPULATE_WRITE keeps the contents, so rows
+// of other callers inside the span are safe).  Without it the copy-back into
+// fresh memory ran at ~5 GB/s, page faults serialising the copy threads
+// (profiles/r02_host_probe.json d2h_pageable_fresh_GBs).  On kernels without
+// MADV_POPULATE_WRITE only the advice is given.
+void prefault_destination(char* lo, char* hi) {
+  constexpr uintptr_t kHuge = 2ull << 20, kPage = 4096;
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(lo) + kHuge - 1) & ~(kHuge - 1);
+  const uintptr_t b = reinterpret_cast<uintptr_t>(hi) & ~(kHuge - 1);
+  if (b > a) (void)madvise(reinterpret_cast<void*>(a), b - a, MADV_HUGEPAGE);
+  const uintptr_t p0 = reinterpret_cast<uintptr_t>(lo) & ~(kPage - 1);
+  const uintptr_t p1 = (reinterpret_cast<uintptr_t>(hi) + kPage - 1) & ~(kPage - 1);
+  if (p1 <= p0) return;
+  static std::atomic<bool> unsupported{false};
+  if (unsupported.load(std::memory_order_relaxed)) return;
+  const int parts = std::max(1, copy_threads());
+  const uintptr_t per = ((p1 - p0) / parts + kHuge - 1) & ~(kHuge - 1);
+  parallel_for(parts, [&](int i) {
+    const uintptr_t s0 = p0 + (uintptr_t)i * per;
+    if (s0 >= p1 || unsupported.load(std::memory_order_relaxed)) return;
+    const uintptr_t s1 = std::min(p1, s0 + per);
+    if (madvise(reinterpret_cast<void*>(s0), s1 - s0, MADV_POPULATE_WRITE) != 0 && errno == EINVAL)
+      unsupported.store(true, std::memory_order_relaxed);
+  });
+}
+
 // $MOA_HOST_TRACE: per staged transfer, time packing vs waiting for slots
 struct StageTrace {
   const bool on = std::getenv("MOA_HOST_TRACE") != nullptr;
-  double pack_ms = 0, wait_ms = 0;
+  double pack_ms = 0, wait_ms = 0, prefault_ms = 0;
   size_t bytes = 0;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
   const char* dir;
@@ -264,8 +299,8 @@ struct StageTrace {
   }
   ~StageTrace() {
     if (on && bytes)
-      fprintf(stderr, "[moa_stage] %s %.1f MiB total=%.2f ms pack=%.2f wait=%.2f -> %.1f GB/s\n", dir,
-              bytes / 1048576.0, since(t0), pack_ms, wait_ms, bytes / since(t0) / 1e6);
+      fprintf(stderr, "[moa_stage] %s %.1f MiB total=%.2f ms pack=%.2f wait=%.2f prefault=%.2f -> %.1f GB/s\n",
+              dir, bytes / 1048576.0, since(t0), pack_ms, wait_ms, prefault_ms, bytes / since(t0) / 1e6);
   }
 };
 
@@ -451,6 +486,16 @@ cudaError_t d2h(int device, void* dst, size_t hpitch, const void* src, size_t dp
   for (size_t c = 0; c < d && c < chunks.size(); c++) issue(c);
   StageTrace tr("d2h");
   tr.bytes = width * rows;
+  static const bool prefault_on = [] {  // $MOA_HOST_PREFAULT=0: off, for comparisons
+    const char* e = std::getenv("MOA_HOST_PREFAULT");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (prefault_on && width * rows >= kPrefaultBytes) {  // while the first chunks are on the link
+    auto t = std::chrono::steady_clock::now();
+    char* lo = static_cast<char*>(dst);
+    prefault_destination(lo, lo + (rows - 1) * hpitch + width);
+    tr.prefault_ms = StageTrace::since(t);
+  }
   for (size_t c = 0; c < chunks.size() && err == cudaSuccess; c++) {
     Slot& s = slots[c % d];
     auto t = std::chrono::steady_clock::now();

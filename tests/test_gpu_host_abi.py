@@ -319,6 +319,28 @@ def test_row_parts_into_page_locked_res(acc, rng):
     assert_bits_equal(got, want, f"outer acc={acc}")
 
 
+def test_large_pageable_result_prefaulted_in_place(rng):
+    """A pageable result of >= 32 MiB is prefaulted before the copy-back
+    (huge-page advice + MADV_POPULATE_WRITE over its span): fresh np.empty
+    memory and a strided row set whose other rows hold data — those rows keep
+    their contents, the set's rows get the device entry's bits."""
+    m, k, n = 13200, 24, 1000   # 106 MB of float64 result; rows 1::3 alone 35 MB
+    a, b = rng.random(m * k) * 2 - 1, rng.random(k * n) * 2 - 1
+    plan = plan_inner((m, k), (k, n))
+    for ops in (moa.MUL_ADD, op_pair("add", "min")):
+        want = _device_result(plan, np.zeros(m * n), a, b, ops)
+        fresh = np.empty(m * n)
+        launch_host(plan, fresh, a, b, ops)
+        assert_bits_equal(fresh, want, f"{ops} fresh")
+        res0 = rng.random(m * n)
+        res = res0.copy()
+        launch_host(plan, res, a, b, ops, start=1, step=3)
+        got, ref = res.reshape(m, n), want.reshape(m, n)
+        assert_bits_equal(got[1::3].ravel(), ref[1::3].ravel(), f"{ops} rows 1::3")
+        keep = np.setdiff1d(np.arange(m), np.arange(1, m, 3))
+        assert_bits_equal(got[keep].ravel(), res0.reshape(m, n)[keep].ravel(), f"{ops} other rows")
+
+
 @pytest.mark.parametrize("acc", [False, True])
 def test_pageable_staging_equals_page_locked(acc, rng):
     """Pageable host buffers above the direct-copy size are staged through
