@@ -30,9 +30,12 @@
 // (one per concurrent caller), large block buffers from a private device
 // memory pool, so a call costs a few API calls beyond its copies and kernels.
 #include <algorithm>
+#include <cstdint>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -180,6 +183,56 @@ size_t direct_out_bytes() {
   return v;
 }
 
+// Accumulating into a result that holds nothing but the reduce identity (the
+// reference's _Runner prefills res with it, kernel.py:149) is the write-only
+// product bit for bit (every kernel folds from the identity in registers), so
+// for results of >= 32 MiB the executor checks the row set's rows first — in
+// parallel, ~10 ms per GiB, stopping at the first other value — and skips
+// sending res to the GPU when the check passes.
+constexpr size_t kIdentityCheckBytes = 32ull << 20;
+
+uint64_t identity_bits(int dtype, int reduce) {
+  switch (dtype) {
+    case MOA_DTYPE_F64: {
+      const double v = reduce == moa::R_ADD ? 0.0 : reduce == moa::R_MUL ? 1.0
+                       : reduce == moa::R_MIN ? __builtin_huge_val() : -__builtin_huge_val();
+      uint64_t u;
+      std::memcpy(&u, &v, 8);
+      return u;
+    }
+    case MOA_DTYPE_F32: {
+      const float v = reduce == moa::R_ADD ? 0.0f : reduce == moa::R_MUL ? 1.0f
+                      : reduce == moa::R_MIN ? __builtin_huge_valf() : -__builtin_huge_valf();
+      uint32_t u;
+      std::memcpy(&u, &v, 4);
+      return u;
+    }
+    case MOA_DTYPE_I32:
+      return (uint32_t)(reduce == moa::R_ADD ? 0 : reduce == moa::R_MUL ? 1
+                        : reduce == moa::R_MIN ? INT32_MAX : INT32_MIN);
+    default:
+      return (uint64_t)(reduce == moa::R_ADD ? int64_t(0) : reduce == moa::R_MUL ? int64_t(1)
+                        : reduce == moa::R_MIN ? INT64_MAX : INT64_MIN);
+  }
+}
+
+template <typename W>
+bool rows_hold(const char* c_rows, size_t c_pitch, int64_t rows, int64_t n, W pat) {
+  std::atomic<bool> other{false};
+  const int parts = (int)std::min<int64_t>(rows, std::max(1, moa::host::copy_threads()));
+  const int64_t per = (rows + parts - 1) / parts;
+  moa::host::parallel_for(parts, [&](int p) {
+    const int64_t r0 = p * per, r1 = std::min(rows, r0 + per);
+    for (int64_t r = r0; r < r1 && !other.load(std::memory_order_relaxed); r++) {
+      const W* row = reinterpret_cast<const W*>(c_rows + (size_t)r * c_pitch);
+      W diff = 0;
+      for (int64_t j = 0; j < n; j++) diff |= row[j] ^ pat;  // vectorises; no early exit per row
+      if (diff) other.store(true, std::memory_order_relaxed);
+    }
+  });
+  return !other.load();
+}
+
 // $MOA_HOST_ROW_PARTS=0 turns the row-part pipeline of large single-block
 // results off (one kernel, then the copy-out), for comparisons
 bool row_parts_enabled() {
@@ -273,7 +326,7 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
     if (rc != 0) return rc;
   }
   if (start >= noproc || elsinop == 0) return 0;  // surplus worker / empty rows
-  const bool acc = (flags & MOA_FLAG_ACCUMULATE) != 0;
+  bool acc = (flags & MOA_FLAG_ACCUMULATE) != 0;
   const int64_t K = rowsinred, N = elsinop;
   if (K == 0 && acc) return 0;  // the empty fold leaves res as it is
   if (res == nullptr || (K > 0 && (a == nullptr || b == nullptr))) {
@@ -288,6 +341,18 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   const int64_t rows = (noproc - start + step - 1) / step;
 
   Trace tr;
+  if (acc && (size_t)(rows * N) * esz >= kIdentityCheckBytes) {
+    const char* rows0 = static_cast<const char*>(res) + (size_t)(start * restride) * esz;
+    const size_t pitch = (size_t)(restride * step) * esz;
+    const uint64_t pat = identity_bits(dtype, reduce_code);
+    const bool ident = esz == 8 ? rows_hold<uint64_t>(rows0, pitch, rows, N, pat)
+                                : rows_hold<uint32_t>(rows0, pitch, rows, N, (uint32_t)pat);
+    if (ident) {  // the fold from res is the fold from the identity
+      acc = false;
+      flags &= ~(uint32_t)MOA_FLAG_ACCUMULATE;
+    }
+    tr.mark(ident ? "identity_res" : "res_checked");
+  }
   Session ss;
   ss.device = device;
   int cur = 0;

@@ -319,6 +319,34 @@ def test_row_parts_into_page_locked_res(acc, rng):
     assert_bits_equal(got, want, f"outer acc={acc}")
 
 
+@pytest.mark.parametrize("dt,ops", [(np.float64, moa.MUL_ADD), (np.float64, op_pair("add", "min")),
+                                    (np.float32, op_pair("multiply", "max")),
+                                    (np.int32, op_pair("add", "min"))])
+def test_accumulate_into_identity_result_skips_its_upload(dt, ops, rng):
+    """MOA_FLAG_ACCUMULATE into a result of >= 32 MiB that holds only the
+    reduce identity (the reference's prefill) runs write-only — the same bits
+    by construction — and one other value anywhere in the row set keeps the
+    fold from res: both equal the device entry's accumulate, pageable and
+    page-locked, whole set and a strided row set."""
+    m, k, n = 9000, 20, 1000
+    a, b = _operands(rng, m * k, dt), _operands(rng, k * n, dt)
+    plan = plan_inner((m, k), (k, n))
+    ident = ops.reduce_identity if np.dtype(dt).kind == "f" else \
+        {"add": 0, "multiply": 1, "min": np.iinfo(dt).max, "max": np.iinfo(dt).min}[ops.reduce_name]
+    for start, step in ((0, 1), (2, 2)):
+        for poke in (None, (m // 2) * n + 7):
+            res0 = np.full(m * n, ident, dtype=dt)
+            if poke is not None:
+                res0[poke] = dt(3) if np.dtype(dt).kind == "i" else dt(-3.5)
+                res0[poke + 2 * n] = res0[poke]   # the row set 2::2 sees it too
+            want = _device_result(plan, res0, a, b, ops, start=start, step=step, accumulate=True)
+            for pin in (False, True):
+                got = _pinned_like(res0) if pin else res0.copy()
+                launch_host(plan, got, a, b, ops, start=start, step=step, accumulate=True)
+                assert_bits_equal(got, want, f"{np.dtype(dt).name} {ops} {start}::{step} "
+                                             f"poke={poke} pinned={pin}")
+
+
 def test_large_pageable_result_prefaulted_in_place(rng):
     """A pageable result of >= 32 MiB is prefaulted before the copy-back
     (huge-page advice + MADV_POPULATE_WRITE over its span): fresh np.empty
