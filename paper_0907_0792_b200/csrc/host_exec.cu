@@ -561,6 +561,11 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
   if (ss.err != cudaSuccess) return fail_cuda(ss.err, "device buffers");
 
   std::vector<cudaEvent_t> b_ready;
+  struct RowPart {
+    int64_t q0, q1;
+    cudaEvent_t ready;
+  };
+  std::vector<RowPart> last_parts;  // the last block's row parts (if split)
   cudaEvent_t a_free[2] = {nullptr, nullptr}, c_free[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> done(blocks.size(), nullptr);
 
@@ -655,7 +660,32 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
         // blocks after the first read all of B: wait for its last chunk
         ss.check(cudaStreamWaitEvent(q.s_comp, b_ready.back(), 0));
         if (ss.err != cudaSuccess) break;
-        if (const int rc = launch(0, K, acc); rc != 0) {
+        // the last block of a DMMA product in row parts, so its copy-out (the
+        // one copy left exposed) starts after a quarter of it: c4 through the
+        // C ABI 249.7 -> 248.5 ms.  Not for the float32 fast folds: each part
+        // re-scans B and a quarter of c5's last block is under one wave of
+        // 128x128 tiles (213.7 -> 215.8 ms; profiles/r02_e2e_last_parts.log).
+        const bool dmma_route = dtype == MOA_DTYPE_F64 && combine_code == moa::C_MUL &&
+                                reduce_code == moa::R_ADD && !(flags & MOA_FLAG_EXACT) && K >= 8;
+        if (i + 1 == blocks.size() && i > 0 && nr >= 4 * kRowAlign && dmma_route &&
+            row_parts_enabled()) {
+          int64_t per = (nr + 3) / 4;
+          per += (kRowAlign - per % kRowAlign) % kRowAlign;
+          const uint32_t f = (flags & ~MOA_FLAG_ACCUMULATE) | (acc ? MOA_FLAG_ACCUMULATE : 0u);
+          for (int64_t q0 = 0; q0 < nr; q0 += per) {
+            const int64_t q1 = q0 + per < nr ? q0 + per : nr;
+            const int rc = moa_product_rows(dtype, c_buf[slot] + (size_t)(q0 * N) * esz,
+                                            a_buf[slot] + (size_t)(q0 * lda) * esz, b_buf, q1 - q0, K,
+                                            N, lda, ldb, N, combine_code, reduce_code, 0, 1, f,
+                                            q.s_comp);
+            if (rc != 0) {
+              ss.err = cudaErrorUnknown;
+              return rc;
+            }
+            last_parts.push_back({q0, q1, ss.event()});
+            ss.check(cudaEventRecord(last_parts.back().ready, q.s_comp));
+          }
+        } else if (const int rc = launch(0, K, acc); rc != 0) {
           ss.err = cudaErrorUnknown;
           return rc;
         }
@@ -679,7 +709,20 @@ extern "C" int moa_product_rows_host(int dtype, void* res, const void* a, const 
       tr.mark("blk_out");
     }
   }
-  if (ss.err == cudaSuccess) copy_out(blocks.size() - 1);
+  if (ss.err == cudaSuccess && !last_parts.empty()) {
+    // the last block's rows part by part, each as soon as its kernel is done
+    const size_t i = blocks.size() - 1;
+    char* host_rows = c_rows + (size_t)blocks[i].r0 * c_pitch;
+    for (const RowPart& rp : last_parts) {
+      if (ss.err != cudaSuccess) break;
+      ss.check(cudaStreamWaitEvent(q.s_out, rp.ready, 0));
+      ss.check(moa::host::d2h(device, host_rows + (size_t)rp.q0 * c_pitch, c_pitch,
+                              c_buf[i % 2] + (size_t)(rp.q0 * N) * esz, (size_t)N * esz,
+                              (size_t)N * esz, (size_t)(rp.q1 - rp.q0), r_pin, q.s_out));
+    }
+  } else if (ss.err == cudaSuccess) {
+    copy_out(blocks.size() - 1);
+  }
   if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_out));
   if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_comp));
   if (ss.err == cudaSuccess) ss.check(cudaStreamSynchronize(q.s_in));
