@@ -67,6 +67,20 @@ struct SemiringShape {
 
 // Default tiles: float32 min/max (c5): 8x8 per thread, two CTAs per SM
 // (tools/tune_semiring.cu); float64 or float64-accumulated: 8x8, one CTA.
+// Unroll of the exact loop's k steps: 4 lets ptxas hoist the next steps'
+// shared loads over the current FP64 work — 4096^3 float64 (add, min) 16.43 ->
+// 14.46 ms, (multiply, max) 15.98 -> 14.35, exact (multiply, add) 10.54 ->
+// 10.06, (min, min) 20.29 -> 18.96, float32 and int32 routes 1-4% faster, all
+// bit-identical — but division (staged reciprocals / multipliers), int64 and
+// the float64 / int32 (min|max, add|multiply) pairs run slower unrolled (f64
+// divide 8.23 -> 9.53 ms, int32 (min, add) -14%), so they keep 1
+// (profiles/r02_tune_semiring_kunroll.jsonl, r02_route_sweep_4096.jsonl,
+// tools/tune_semiring_kunroll.cu, tools/route_sweep.py).
+#ifndef MOA_SEMIRING_KUNROLL
+#define MOA_SEMIRING_KUNROLL 4
+#endif
+constexpr int KUNROLL = MOA_SEMIRING_KUNROLL;
+
 template <typename T, int C, int R> struct DefaultTile {
   static constexpr bool F4 = sizeof(typename AccType<T, C, R>::type) == 4;
   static constexpr int TM = 8, TN = 8, MINB = F4 ? 2 : 1;
@@ -247,6 +261,10 @@ __global__ void __launch_bounds__(SNT, MINB)
       // A elements are warp-broadcast loads; the B elements of columns
       // 16j + tx sit one k-pair apart, so a warp's 16 loads per j span 128
       // (float) or 256 (double) contiguous bytes.
+      constexpr bool MINMAX_SUM = (C == C_MIN || C == C_MAX) && (R == R_ADD || R == R_MUL) &&
+                                  !std::is_same<T, float>::value;
+      constexpr int KU = (C == C_DIV || std::is_same<T, int64_t>::value || MINMAX_SUM) ? 1 : KUNROLL;
+#pragma unroll KU
       for (int kk = 0; kk < kend; kk++) {
         const T* ak = reinterpret_cast<const T*>(as + (kk >> 1) * BM + ty * TM) + (kk & 1);
         const T* bk = reinterpret_cast<const T*>(bs + (kk >> 1) * BN + (PAIRED ? 2 * tx : tx)) + (kk & 1);

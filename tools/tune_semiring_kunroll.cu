@@ -1,0 +1,78 @@
+// The exact semiring kernel (csrc/semiring_impl.cuh, default 8x8 tiles) with
+// its k loop unrolled MOA_SEMIRING_KUNROLL times: float64 routes at 4096^3
+// and float32 (add, min) exact, CUDA-event times and bits against a
+// reference launch of the same build (tools; not part of the library).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//        -DMOA_SEMIRING_KUNROLL=2 -o tools/tune_semiring_kunroll tools/tune_semiring_kunroll.cu
+#include "../paper_0907_0792_b200/csrc/semiring_impl.cuh"
+#include "../paper_0907_0792_b200/csrc/tma.cu"
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+std::atomic<uint64_t> moa::g_launches{0};
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+  fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1);} } while (0)
+
+template <typename T>
+__global__ void fill(T* p, size_t n, unsigned long long seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
+    p[i] = T((double)(x >> 11) * 0x1.0p-53 * 100.0 - 30.0) + T(std::is_integral<T>::value && ((x >> 7) & 63) == 0 ? 0 : 0);
+  }
+}
+
+template <typename T, int C, int R>
+void trial(const char* route, int64_t n) {
+  T *a, *b, *c;
+  CK(cudaMalloc(&a, n * n * sizeof(T))); CK(cudaMalloc(&b, n * n * sizeof(T)));
+  CK(cudaMalloc(&c, n * n * sizeof(T)));
+  fill<<<1184, 256>>>(a, n * n, 1); fill<<<1184, 256>>>(b, n * n, 2);
+  const int dt = std::is_same<T, double>::value ? MOA_DTYPE_F64 : std::is_same<T, float>::value ? MOA_DTYPE_F32
+               : std::is_same<T, int32_t>::value ? MOA_DTYPE_I32 : MOA_DTYPE_I64;
+  moa::Problem p{dt, c, a, b, n, n, n, n, n, n, C, R, false, 0};
+  cudaEvent_t s, e;
+  CK(cudaEventCreate(&s)); CK(cudaEventCreate(&e));
+  CK((moa::semiring_launch<T, C, R, false, -1>(p, nullptr)));
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 3; r++) {
+    CK(cudaEventRecord(s));
+    CK((moa::semiring_launch<T, C, R, false, -1>(p, nullptr)));
+    CK(cudaEventRecord(e)); CK(cudaEventSynchronize(e));
+    float ms; CK(cudaEventElapsedTime(&ms, s, e)); best = ms < best ? ms : best;
+  }
+  // checksum of the bits (compared across builds by the caller)
+  std::vector<T> h(n * n);
+  CK(cudaMemcpy(h.data(), c, n * n * sizeof(T), cudaMemcpyDeviceToHost));
+  unsigned long long sum = 0;
+  for (int64_t i = 0; i < n * n; i++) {
+    unsigned long long u = 0;
+    std::memcpy(&u, &h[i], sizeof(T));
+    sum = sum * 1099511628211ull + u;
+  }
+  printf("{\"kunroll\": %d, \"route\": \"%s\", \"n\": %lld, \"ms\": %.3f, \"Gpairs_s\": %.1f, \"bits_hash\": \"%016llx\"}\n",
+         moa::KUNROLL, route, (long long)n, best, (double)n * n * n / (best * 1e-3) / 1e9, sum);
+  fflush(stdout);
+  CK(cudaFree(a)); CK(cudaFree(b)); CK(cudaFree(c));
+}
+
+int main() {
+  trial<double, 2, 0>("f64_mul_add_exact", 4096);
+  trial<double, 0, 0>("f64_add_add", 4096);
+  trial<double, 0, 2>("f64_add_min", 4096);
+  trial<double, 2, 3>("f64_mul_max", 4096);
+  trial<double, 4, 2>("f64_min_min", 4096);
+  trial<float, 0, 0>("f32_add_add", 4096);
+  trial<float, 4, 3>("f32_min_max", 4096);
+  trial<double, 3, 0>("f64_div_add", 2048);
+  trial<float, 3, 2>("f32_div_min", 2048);
+  trial<int32_t, 2, 0>("i32_mul_add", 4096);
+  trial<int32_t, 0, 3>("i32_add_max", 4096);
+  trial<int64_t, 0, 2>("i64_add_min", 2048);
+  trial<int64_t, 3, 2>("i64_div_min", 2048);
+  return 0;
+}
