@@ -50,7 +50,12 @@ struct SemiringShape {
   static constexpr bool F4 = sizeof(typename AccType<T, C, R>::type) == 4;
   static constexpr int TM = TM_, TN = TN_;
   static constexpr int BM = 16 * TM, BN = 16 * TN;
-  static constexpr int BK = F4 ? 32 : 16;       // k per stage (one barrier per BK)
+  // k per stage (one barrier per BK): 32 for 4-byte accumulators and for
+  // float64 data (4096^3 exact (multiply, add) 10.06 -> 9.74 ms, sums -3%,
+  // compare-select -1..-2%; profiles/r02_tune_semiring_kunroll.jsonl); 16 for
+  // float32 data summed in float64, int64, and division, whose staged divisor
+  // tables would not fit three 32-deep stages
+  static constexpr int BK = F4 ? 32 : (std::is_same<T, double>::value && C != C_DIV) ? 32 : 16;
   static constexpr int KP = BK / 2;             // k-pairs per stage
   static constexpr int STAGES = 3;
   static constexpr int A_STAGE = KP * BM;       // pairs
