@@ -72,6 +72,7 @@ int main() {
   CK(cudaMalloc(&c, n * n * 8)); CK(cudaMalloc(&ref, n * n * 8)); CK(cudaMalloc(&cnt, 8));
   fill<<<1184, 256>>>(a, n * n, 1); fill<<<1184, 256>>>(b, n * n, 2);
   moa::Problem p{MOA_DTYPE_F64, ref, a, b, n, n, n, n, n, n, 0, 0, false, 0};
+  sweep<2, 0>("mul_add_exact", p, c, ref, cnt);
   sweep<0, 0>("add_add", p, c, ref, cnt);
   sweep<0, 2>("add_min", p, c, ref, cnt);
   sweep<2, 3>("mul_max", p, c, ref, cnt);
