@@ -67,6 +67,8 @@ int main() {
   trial<double, 2, 3>("f64_mul_max", 4096);
   trial<double, 4, 2>("f64_min_min", 4096);
   trial<float, 0, 0>("f32_add_add", 4096);
+  trial<float, 2, 0>("f32_mul_add", 4096);
+  trial<float, 2, 2>("f32_mul_min", 4096);
   trial<float, 4, 3>("f32_min_max", 4096);
   trial<double, 3, 0>("f64_div_add", 2048);
   trial<float, 3, 2>("f32_div_min", 2048);
