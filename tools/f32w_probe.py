@@ -1,7 +1,9 @@
 """float32 pairs folded in float64 through the production route at 4096^3 —
-(x,+), (+,+), (x,min), (min,+), (x,x) — CUDA-event time per launch, for
-comparing $MOA_F32W=1 (register-staged float64 tiles) with $MOA_F32W=0 (tools
-probe; not a test).  Usage: python tools/f32w_probe.py [n]"""
+(x,+), (+,+), (x,min), (min,+), (x,x) — CUDA-event time per launch (tools
+probe; not a test).  Round 2 used it with $MOA_F32W to compare a
+register-staged float64-tile kernel that was then dropped
+(profiles/r02_tune_semiring_kunroll.jsonl); the variable no longer selects
+anything.  Usage: python tools/f32w_probe.py [n]"""
 import os
 import sys
 from pathlib import Path
